@@ -1,0 +1,200 @@
+/* kvflow.h -- C-ABI of the B200-native KVFlow KV-movement engine (libkvflow.so).
+ *
+ * This is the drop-in boundary.  The reference (kvsim, C++) models the
+ * tier engine's transfers with a cost model and never moves bytes; every entry point
+ * below replaces one modelled step of that engine with real sm_100a work:
+ *
+ *   kvf_h2d_gather        <- TierManager::begin_load     proj/src/tier_manager.cpp:61-77
+ *                            (+ enqueue_job, tier_manager.cpp:35-46)           [K1]
+ *   kvf_d2h_scatter       <- TierManager::begin_offload  proj/src/tier_manager.cpp:48-59 [K2]
+ *   kvf_dev_gather/
+ *   kvf_dev_scatter       <- (new) staged path / compaction, SURVEY §8a row A13      [K3]
+ *   kvf_job_query/wait    <- TierManager::complete        proj/src/tier_manager.cpp:95-124
+ *                            (the TransferDone event, scheduler.cpp:94-97)
+ *   kvf_priority_propagate<- RadixCache::set_agent_priorities proj/src/radix_cache.cpp:266-285 [K4]
+ *   kvf_victim_select     <- RadixCache::evict (selection) proj/src/radix_cache.cpp:302-372 [K5]
+ *   kvf_slots_alloc/free  <- (new) token-slot pools; the reference keeps only a byte ledger
+ *                            (GpuPool, proj/include/kvsim/tier_manager.hpp:38-46)
+ *
+ * Conventions: every function is extern "C", never throws, and returns an int status:
+ * KVF_OK (0) or a code that maps 1:1 onto kvsim::ErrorCode (errors.hpp:8-28) as
+ * (ErrorCode + 1), plus engine-specific codes >= 100.  kvf_last_error() gives the text of
+ * the last failure on the calling thread.  No torch types cross this boundary.
+ *
+ * KV layout (both tiers, per engine = per GPU shard):
+ *   pool[plane = layer*2 + (0:K|1:V)][token_slot][local kv head][head_dim]  (bf16)
+ * so one token of one plane is  tpb = kv_heads_local * head_dim * dtype_bytes  contiguous
+ * bytes, and a node is a list of token-slot runs.  Splitting a radix node at any token
+ * offset (radix_cache.cpp:142-177, 226-259) splits its run list; no bytes move.
+ */
+#ifndef KVFLOW_H
+#define KVFLOW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------------- */
+enum {
+    KVF_OK = 0,
+    /* kvsim::ErrorCode + 1 (proj/include/kvsim/errors.hpp:8-28) */
+    KVF_E_UNKNOWN_AGENT = 1,
+    KVF_E_SELF_LOOP = 2,
+    KVF_E_DUPLICATE_AGENT = 3,
+    KVF_E_EMPTY_ACTIVE_SET = 4,
+    KVF_E_UNDERFLOW_UNLOCK = 5,
+    KVF_E_UNKNOWN_BOUNDARY_NODE = 6,
+    KVF_E_BOUNDARY_BEYOND_CACHE = 7,
+    KVF_E_INSUFFICIENT_HISTORY = 8,
+    KVF_E_ILLEGAL_STATE = 9,
+    KVF_E_OUT_OF_GPU_MEMORY = 10,
+    KVF_E_CONFIG = 11,
+    KVF_E_UNKNOWN_AXIS = 12,
+    KVF_E_IO = 13,
+    KVF_E_INTERNAL = 14,
+    /* engine-specific */
+    KVF_E_CUDA = 100,          /* a CUDA runtime call failed (text in kvf_last_error) */
+    KVF_E_INVALID_ARG = 101,
+    KVF_E_OUT_OF_HOST_SLOTS = 102,
+    KVF_E_NO_DEVICE = 103,     /* no CUDA device: the engine never falls back to the CPU */
+    KVF_E_UNKNOWN_JOB = 104,
+    KVF_E_TOO_LARGE = 105
+};
+
+enum { KVF_TIER_DEVICE = 0, KVF_TIER_HOST = 1 };
+
+/* copy back-ends for K1/K2 (PCIe).  K3 always uses the SM path. */
+enum {
+    KVF_COPY_SM_VEC = 0,  /* LDG.128 / STG.128 SM-driven zero-copy (host pool is mapped pinned) */
+    KVF_COPY_SM_BULK = 1, /* cp.async.bulk (TMA bulk engine) staging through shared memory      */
+    KVF_COPY_CE = 2       /* copy engine (cudaMemcpy2DAsync per piece) -- comparator only      */
+};
+
+typedef struct kvf_engine kvf_engine; /* opaque */
+
+typedef struct {
+    uint32_t layers;         /* L                                   */
+    uint32_t kv_heads_total; /* Hkv of the model                    */
+    uint32_t kv_heads_local; /* heads this shard holds (Hkv / G)    */
+    uint32_t head_offset;    /* first global head of this shard     */
+    uint32_t head_dim;       /* D                                   */
+    uint32_t dtype_bytes;    /* 2 (bf16)                            */
+} kvf_geometry;
+
+typedef struct {
+    int32_t device;           /* CUDA ordinal                                          */
+    uint64_t gpu_slots;       /* HBM pool capacity in tokens                           */
+    uint64_t host_slots;      /* pinned host pool capacity in tokens                   */
+    uint32_t pcie_ctas;       /* grid for K1/K2 (0 = default)                          */
+    uint32_t pcie_mode;       /* KVF_COPY_* for K1/K2                                  */
+    uint32_t hbm_ctas;        /* grid for K3 (0 = default: 4 per SM)                   */
+    int32_t host_numa_node;   /* -1: no binding; else mbind the host pool to this node */
+} kvf_engine_config;
+
+typedef struct {
+    uint64_t start; /* first token slot */
+    uint64_t len;   /* tokens           */
+} kvf_run;
+
+/* ---- lifecycle -------------------------------------------------------------------- */
+const char* kvf_last_error(void);
+const char* kvf_version(void);
+int kvf_device_count(int32_t* out);
+int kvf_engine_create(const kvf_geometry* geom, const kvf_engine_config* cfg, kvf_engine** out);
+int kvf_engine_destroy(kvf_engine* e);
+/* bytes one token occupies in one plane on this shard, and across all planes */
+int kvf_engine_token_bytes(const kvf_engine* e, uint64_t* tpb, uint64_t* token_bytes);
+int kvf_engine_set_copy_mode(kvf_engine* e, uint32_t pcie_mode, uint32_t pcie_ctas, uint32_t hbm_ctas);
+
+/* ---- token-slot pools ---------------------------------------------------------------- */
+/* Allocates `tokens` slots as <= max_runs runs (best-fit single run when possible). */
+int kvf_slots_alloc(kvf_engine* e, int32_t tier, uint64_t tokens, kvf_run* out_runs, uint32_t max_runs,
+                    uint32_t* n_runs);
+int kvf_slots_free(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs);
+int kvf_slots_free_count(const kvf_engine* e, int32_t tier, uint64_t* free_tokens, uint64_t* free_runs);
+/* Raw pool base (device pointer for DEVICE; host pointer -- also device-addressable -- for HOST). */
+int kvf_pool_ptr(const kvf_engine* e, int32_t tier, void** base, uint64_t* slots);
+
+/* ---- data movement (async; one job = one node transfer) ------------------------------- */
+/* job_id is chosen by the caller (TierManager job ids, tier_manager.cpp:470-481) and must be
+ * unique among unreleased jobs.  Token k of the node (in run order) moves from the k-th slot
+ * of src_runs to the k-th slot of dst_runs, all planes; total src and dst tokens must match. */
+int kvf_h2d_gather(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
+                   const kvf_run* dev_runs, uint32_t n_dev); /* K1 */
+int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint32_t n_dev,
+                    const kvf_run* host_runs, uint32_t n_host); /* K2 */
+/* K3: paged HBM pool <-> contiguous HBM staging laid out [plane][token][head][dim]
+ * (a 1-run pool of `tokens` slots).  staging is a device pointer. */
+int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint32_t n_dev, void* staging);
+int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* dev_runs,
+                    uint32_t n_dev);
+
+/* fences (TierManager::complete): 1 in *done when the job's bytes have landed */
+int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done);
+int kvf_job_wait(kvf_engine* e, uint64_t job_id);
+/* device duration of the job's kernel(s), CUDA events on the job's own stream */
+int kvf_job_elapsed_ms(kvf_engine* e, uint64_t job_id, float* ms);
+int kvf_job_release(kvf_engine* e, uint64_t job_id);
+int kvf_sync_all(kvf_engine* e);
+
+/* ---- decisions (synchronous; small SoA in, ordered actions out) ------------------------- */
+/* SoA view of the radix tree, index 0 = root (parent -1), parent[i] < i (preorder). */
+typedef struct {
+    uint32_t n;
+    const int32_t* parent;
+    const uint16_t* depth;   /* root = 0 */
+    const uint8_t* status;   /* 0 IN_GPU 1 BACKUP_IN_CPU 2 LOADING 3 OFFLOADING (radix_cache.hpp:21-28) */
+    const int32_t* lock;
+    const int64_t* rank;
+    const double* time;      /* LastAccess.time (radix_cache.hpp:44-47) */
+    const uint64_t* seq;     /* LastAccess.seq */
+    const uint64_t* id;
+    const uint64_t* tokens;
+    const uint8_t* backed;   /* cpu_backed */
+    uint64_t bytes_per_token;
+} kvf_tree_view;
+
+typedef struct {
+    uint64_t needed;
+    int32_t workflow_aware; /* EvictionPolicy::WorkflowAware */
+    int32_t offload_mode;   /* TierMode::Offload */
+    int32_t has_floor;      /* EvictRequest::rank_floor_exclusive engaged */
+    int64_t floor;
+    uint64_t cpu_used;      /* TierManager::cpu_used()      */
+    uint64_t cpu_capacity;  /* 0 = unbounded                */
+} kvf_evict_request;
+
+enum { KVF_ACT_OFFLOAD = 0, KVF_ACT_DISCARD_TO_BACKUP = 1, KVF_ACT_REMOVE = 2 };
+
+/* K4: out_rank[i] for i >= 1 = min(SUFFIX, min over boundaries b whose root path contains i
+ * of cand_rank[b]).  out_rank[0] = SUFFIX. */
+int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, const int32_t* boundary_idx,
+                           const int64_t* cand_rank, uint32_t m, int64_t* out_rank);
+/* K5: the ordered victims the reference's greedy heap would pop, with their actions. */
+int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_request* req, int32_t* out_idx,
+                      uint8_t* out_action, uint32_t* out_count, uint64_t* out_immediate, uint64_t* out_pending);
+
+/* ---- payload (prefill emulation) and verification ----------------------------------- */
+/* Writes the deterministic payload of tokens with content ids cids[0..ntok) into the runs
+ * (emulates prefill writing KV).  Async on the engine's compute stream. */
+int kvf_fill_payload(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs, const uint64_t* cids,
+                     uint64_t ntok);
+/* Order-independent checksum of a node's bytes in logical (plane, token, byte) order.  Sync. */
+int kvf_checksum(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs, uint64_t* out);
+/* Copies a node's bytes in logical order into a host buffer of ntok*token_bytes bytes.  Sync. */
+int kvf_read_runs(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs, void* dst, uint64_t dst_bytes);
+
+/* ---- stats ---------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t kernel_launches; /* every kernel this engine launched */
+    uint64_t h2d_bytes, d2h_bytes, dev_bytes;
+    uint64_t h2d_jobs, d2h_jobs, dev_jobs, decisions;
+} kvf_stats;
+int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVFLOW_H */

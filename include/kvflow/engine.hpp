@@ -1,0 +1,75 @@
+// kvflow host API -- RAII C++ handle over the CUDA engine's C-ABI (include/kvflow.h).
+// The host control plane (RadixCache, TierManager) talks to the GPU only through this.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "kvflow.h"
+#include "kvflow/errors.hpp"
+
+namespace kvf {
+
+using Run = kvf_run;
+using RunList = std::vector<Run>;
+
+inline uint64_t run_tokens(const RunList& r) {
+    uint64_t t = 0;
+    for (const Run& x : r) t += x.len;
+    return t;
+}
+
+// Split `runs` after `tokens` tokens: returns the head, leaves the tail in `runs`.
+RunList split_runs(RunList& runs, uint64_t tokens);
+
+// Maps an engine status onto the reference's ErrorCode convention (code = status - 1).
+[[noreturn]] void throw_engine(int status, const std::string& what);
+
+struct EngineOptions {
+    uint32_t layers = 32, kv_heads_total = 8, kv_heads_local = 8, head_offset = 0, head_dim = 128;
+    int device = 0;
+    uint64_t gpu_slots = 0, host_slots = 0;
+    uint32_t pcie_mode = KVF_COPY_SM_VEC, pcie_ctas = 0, hbm_ctas = 0;
+    int numa_node = -1;
+};
+
+class Engine {
+public:
+    explicit Engine(const EngineOptions& opt);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    kvf_engine* raw() const { return e_; }
+    uint64_t token_bytes() const { return token_bytes_; }
+    const EngineOptions& options() const { return opt_; }
+
+    RunList alloc(int tier, uint64_t tokens);
+    void free(int tier, const RunList& runs);
+    uint64_t free_tokens(int tier) const;
+
+    void h2d(uint64_t job, const RunList& host, const RunList& dev);
+    void d2h(uint64_t job, const RunList& dev, const RunList& host);
+    bool query(uint64_t job);
+    void wait(uint64_t job);
+    float elapsed_ms(uint64_t job);
+    void release(uint64_t job);
+    void sync();
+
+    void fill(int tier, const RunList& runs, const std::vector<uint64_t>& cids);
+    uint64_t checksum(int tier, const RunList& runs);
+
+    std::vector<int64_t> priorities(const std::vector<int32_t>& parent, const std::vector<int32_t>& bidx,
+                                    const std::vector<int64_t>& cand);
+    void victims(const kvf_tree_view& tree, const kvf_evict_request& req, std::vector<int32_t>& idx,
+                 std::vector<uint8_t>& action, uint64_t& immediate, uint64_t& pending);
+    kvf_stats stats() const;
+
+private:
+    kvf_engine* e_ = nullptr;
+    EngineOptions opt_;
+    uint64_t token_bytes_ = 0;
+};
+
+}  // namespace kvf

@@ -1,0 +1,195 @@
+// kvflow host API -- token-segment radix cache (reference: proj/include/kvsim/radix_cache.hpp:1-196).
+//
+// Same public surface as the reference RadixCache (match_prefix, peek_prefix, insert,
+// lock/unlock_root_path, mark_fixed_boundary, boundary_node, set_agent_priorities, evict,
+// dump, for_each_node, node_count, gpu_resident_bytes), plus the B200 data plane:
+//   * every node carries the token-slot runs of its KV on each tier (dev_runs, host_runs);
+//     splits at any token offset split the run lists (no bytes move);
+//   * insert() gives new nodes HBM slots and writes their payload (prefill emulation);
+//   * set_agent_priorities() runs on the GPU (K4) and evict() takes its victim order from
+//     the GPU (K5) -- the tree is packed as a preorder SoA and shipped per call.
+// Without an attached Engine the tree still works as a host structure, but priorities and
+// eviction throw ErrorCode::NoDevice (there is no CPU decision path).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <optional>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kvflow/engine.hpp"
+#include "kvflow/errors.hpp"
+#include "kvflow/types.hpp"
+
+namespace kvf {
+
+class TierManager;
+
+enum class NodeStatus : uint8_t { InGpu = 0, BackupInCpu = 1, Loading = 2, Offloading = 3 };
+const char* status_name(NodeStatus s);
+bool is_legal_transition(NodeStatus from, NodeStatus to);
+
+// Eviction rank: larger = more evictable (radix_cache.hpp:30-38 of the reference).
+inline constexpr int64_t kRankUnreachable = std::numeric_limits<int64_t>::max() / 4;
+inline constexpr int64_t kRankSuffix = std::numeric_limits<int64_t>::max() / 2;
+inline int64_t rank_for_step(StepValue s) { return s == kStepUnreachable ? kRankUnreachable : s; }
+std::string rank_label(int64_t rank);
+
+enum class EvictionPolicy { Lru, WorkflowAware };
+enum class TierMode { Discard, Offload };
+
+struct LastAccess {
+    VirtualTime time = 0;
+    uint64_t seq = 0;
+};
+
+struct CacheNode {
+    uint64_t id = 0;
+    CacheNode* parent = nullptr;
+    std::map<TokenId, std::unique_ptr<CacheNode>> children;  // by first token of the child key
+    TokenSeq key;
+    NodeStatus status = NodeStatus::InGpu;
+    int64_t rank = kRankSuffix;
+    LastAccess last_access;
+    int lock_count = 0;
+    bool cpu_backed = false;
+    bool prefetched_unused = false;
+    std::set<AgentId> fixed_boundary_for;
+
+    // ---- data plane ----
+    RunList dev_runs;       // HBM token slots (InGpu / Offloading; Loading = destination)
+    RunList host_runs;      // pinned host token slots (cpu_backed, or Offloading destination)
+    uint64_t prefix_cid = 0;  // content id of the token before key[0] (payload identity)
+    uint64_t end_cid = 0;     // content id of key.back()
+
+    size_t token_count() const { return key.size(); }
+    bool is_root() const { return parent == nullptr; }
+    bool has_device_child() const;
+};
+
+struct MatchResult {
+    size_t matched_tokens = 0;
+    std::vector<CacheNode*> path;
+    CacheNode* partial = nullptr;
+    size_t partial_len = 0;
+    std::vector<CacheNode*> needed_nodes() const;
+};
+
+struct InsertResult {
+    std::vector<CacheNode*> path;
+    Bytes new_bytes = 0;
+    size_t new_nodes = 0;
+};
+
+struct EvictedVictim {
+    uint64_t node_id = 0;
+    Bytes bytes = 0;
+    bool immediate = false;
+};
+
+struct EvictOutcome {
+    std::vector<EvictedVictim> victims;
+    Bytes immediate_freed = 0;
+    Bytes pending_freed = 0;
+    bool sufficient = false;
+};
+
+struct EvictRequest {
+    Bytes needed = 0;
+    EvictionPolicy policy = EvictionPolicy::Lru;
+    TierMode mode = TierMode::Discard;
+    std::optional<int64_t> rank_floor_exclusive;
+};
+
+// Content id chain: cid(token i) = mix(cid(token i-1), token i).  Root seed below.
+inline constexpr uint64_t kRootCid = 0x6b766600ULL;
+uint64_t next_cid(uint64_t prev, TokenId token);
+
+class RadixCache {
+public:
+    explicit RadixCache(Bytes bytes_per_token, Engine* engine = nullptr);
+    ~RadixCache();
+
+    Bytes bytes_per_token() const { return bpt_; }
+    CacheNode& root() { return *root_; }
+    const CacheNode& root() const { return *root_; }
+    Bytes node_bytes(const CacheNode& n) const { return n.token_count() * bpt_; }
+    Engine* engine() const { return engine_; }
+    void attach_engine(Engine* e);
+
+    MatchResult match_prefix(const TokenSeq& tokens, VirtualTime now);
+    MatchResult peek_prefix(const TokenSeq& tokens) const;
+    InsertResult insert(const TokenSeq& tokens, VirtualTime now);
+    void lock_root_path(CacheNode* deepest);
+    void unlock_root_path(CacheNode* deepest);
+    CacheNode* mark_fixed_boundary(const AgentId& agent, const TokenSeq& tokens, size_t fixed_len);
+    CacheNode* boundary_node(const AgentId& agent) const;
+
+    // K4 on the GPU: every node SUFFIX, then min(rank_for_step) along boundary root paths.
+    void set_agent_priorities(const StepMap& steps);
+    // K5 on the GPU picks the ordered victims; the host applies each action through `tier`.
+    EvictOutcome evict(const EvictRequest& req, TierManager& tier, VirtualTime now);
+
+    std::string dump() const;
+    template <typename F>
+    void for_each_node(F&& f) const {
+        // preorder, children in first-token order (same walk as the reference's for_each_impl)
+        std::vector<const CacheNode*> stack;
+        for (auto it = root_->children.rbegin(); it != root_->children.rend(); ++it) stack.push_back(it->second.get());
+        while (!stack.empty()) {
+            const CacheNode* n = stack.back();
+            stack.pop_back();
+            f(*n);
+            for (auto it = n->children.rbegin(); it != n->children.rend(); ++it) stack.push_back(it->second.get());
+        }
+    }
+    size_t node_count() const;
+    Bytes gpu_resident_bytes() const;
+
+    // Content ids of every token of n (walks the prefix chain of its key).
+    std::vector<uint64_t> node_cids(const CacheNode& n) const;
+    // Decision-call statistics (wall time of K4/K5 round trips, host pack time).
+    struct DecisionStats {
+        uint64_t priority_calls = 0, evict_calls = 0;
+        double priority_us = 0, evict_us = 0, pack_us = 0;
+    };
+    const DecisionStats& decision_stats() const { return dstats_; }
+
+private:
+    friend class TierManager;
+    CacheNode* new_node(CacheNode* parent, TokenSeq key, VirtualTime now);
+    void touch(CacheNode& n, VirtualTime now);
+    CacheNode* split_node(CacheNode* node, size_t offset);
+    void remove_node(CacheNode* node);
+    void drop_boundary_markers(CacheNode* node);
+    void require_engine(const char* what) const;
+    // preorder SoA snapshot for K4/K5
+    void pack(bool full);
+
+    Bytes bpt_;
+    Engine* engine_ = nullptr;
+    std::unique_ptr<CacheNode> root_;
+    uint64_t next_id_ = 1;
+    uint64_t touch_counter_ = 0;
+    std::unordered_map<AgentId, CacheNode*, AgentIdHash> boundaries_;
+
+    struct Soa {
+        std::vector<CacheNode*> node;
+        std::vector<int32_t> parent, lock;
+        std::vector<uint16_t> depth;
+        std::vector<uint8_t> status, backed;
+        std::vector<int64_t> rank;
+        std::vector<double> time;
+        std::vector<uint64_t> seq, id, tokens;
+        std::unordered_map<const CacheNode*, int32_t> index;
+    } soa_;
+    DecisionStats dstats_;
+};
+
+size_t update_fixed_heuristic(const std::vector<size_t>& hit_lengths, size_t window = 4);
+
+}  // namespace kvf

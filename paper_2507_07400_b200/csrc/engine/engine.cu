@@ -1,0 +1,921 @@
+// libkvflow.so -- B200-native KV-movement engine (pools, jobs, K1/K2/K3 copy kernels,
+// payload fill + checksum).  Decisions (K4/K5) live in decide.cu.
+//
+// Replaces the modelled transfers of the reference tier engine
+// (proj/src/tier_manager.cpp:35-124): there a TransferJob's completion time is
+// bytes/(bw*eff)+latency; here a job is a real sm_100a kernel on a dedicated copy stream
+// bracketed by CUDA events, and "completion" is the stop event.
+#include <cuda_runtime.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "engine_internal.hpp"
+
+using namespace kvf_impl;
+
+// =====================================================================================
+// errors
+// =====================================================================================
+namespace kvf_impl {
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char* what) {
+    return set_error(KVF_E_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+// =====================================================================================
+// slot allocator
+// =====================================================================================
+void SlotAllocator::reset(uint64_t slots) {
+    by_start_.clear();
+    by_len_.clear();
+    capacity_ = slots;
+    free_tokens_ = 0;
+    if (slots) insert_free(0, slots);
+}
+
+void SlotAllocator::insert_free(uint64_t start, uint64_t len) {
+    by_start_.emplace(start, len);
+    by_len_.emplace(len, start);
+    free_tokens_ += len;
+}
+
+void SlotAllocator::erase_free(std::map<uint64_t, uint64_t>::iterator it) {
+    auto range = by_len_.equal_range(it->second);
+    for (auto j = range.first; j != range.second; ++j)
+        if (j->second == it->first) {
+            by_len_.erase(j);
+            break;
+        }
+    free_tokens_ -= it->second;
+    by_start_.erase(it);
+}
+
+bool SlotAllocator::alloc(uint64_t tokens, std::vector<kvf_run>& out) {
+    out.clear();
+    if (tokens == 0) return true;
+    if (tokens > free_tokens_) return false;
+    // best fit: smallest free run that holds everything -> one run, no fragmentation
+    auto fit = by_len_.lower_bound(tokens);
+    if (fit != by_len_.end()) {
+        uint64_t start = fit->second, len = fit->first;
+        erase_free(by_start_.find(start));
+        out.push_back({start, tokens});
+        if (len > tokens) insert_free(start + tokens, len - tokens);
+        return true;
+    }
+    // otherwise take the largest runs first (fewest pieces for the copy kernels)
+    uint64_t need = tokens;
+    while (need > 0) {
+        auto big = std::prev(by_len_.end());
+        uint64_t start = big->second, len = big->first;
+        erase_free(by_start_.find(start));
+        uint64_t take = std::min(len, need);
+        out.push_back({start, take});
+        if (len > take) insert_free(start + take, len - take);
+        need -= take;
+    }
+    return true;
+}
+
+bool SlotAllocator::release(const kvf_run& r) {
+    if (r.len == 0) return true;
+    if (r.start + r.len > capacity_ || r.start + r.len < r.start) return false;
+    uint64_t start = r.start, len = r.len;
+    auto next = by_start_.lower_bound(start);
+    if (next != by_start_.end() && next->first < start + len) return false;  // overlaps a free run
+    if (next != by_start_.begin()) {
+        auto prev = std::prev(next);
+        if (prev->first + prev->second > start) return false;
+        if (prev->first + prev->second == start) {  // coalesce left
+            start = prev->first;
+            len += prev->second;
+            erase_free(prev);
+        }
+    }
+    next = by_start_.lower_bound(start + len);
+    if (next != by_start_.end() && next->first == start + len) {  // coalesce right
+        len += next->second;
+        erase_free(next);
+    }
+    insert_free(start, len);
+    return true;
+}
+
+void merge_runs(const kvf_run* a, uint32_t na, const kvf_run* b, uint32_t nb, std::vector<Piece>& out) {
+    out.clear();
+    uint32_t i = 0, j = 0;
+    uint64_t ao = 0, bo = 0;
+    while (i < na && j < nb) {
+        uint64_t l = std::min(a[i].len - ao, b[j].len - bo);
+        if (l) {
+            if (!out.empty() && out.back().src_slot + out.back().ntok == a[i].start + ao &&
+                out.back().dst_slot + out.back().ntok == b[j].start + bo)
+                out.back().ntok += l;  // adjacent on both sides: one piece
+            else
+                out.push_back({a[i].start + ao, b[j].start + bo, l});
+        }
+        ao += l;
+        bo += l;
+        if (ao == a[i].len) { ++i; ao = 0; }
+        if (bo == b[j].len) { ++j; bo = 0; }
+    }
+}
+
+int Workspace::ensure(size_t dn, size_t hn) {
+    if (dn > dev_bytes) {
+        if (dev) cudaFree(dev);
+        dev = nullptr;
+        size_t sz = std::max(dn, dev_bytes * 2);
+        KVF_CUDA(cudaMalloc(&dev, sz));
+        dev_bytes = sz;
+    }
+    if (hn > host_bytes) {
+        if (host) cudaFreeHost(host);
+        host = nullptr;
+        size_t sz = std::max(hn, host_bytes * 2);
+        KVF_CUDA(cudaHostAlloc(&host, sz, cudaHostAllocDefault));
+        host_bytes = sz;
+    }
+    return KVF_OK;
+}
+
+void Workspace::release() {
+    if (dev) cudaFree(dev);
+    if (host) cudaFreeHost(host);
+    dev = host = nullptr;
+    dev_bytes = host_bytes = 0;
+}
+
+int acquire_event(kvf_engine* e, cudaEvent_t* ev) {
+    if (!e->event_pool.empty()) {
+        *ev = e->event_pool.back();
+        e->event_pool.pop_back();
+        return KVF_OK;
+    }
+    KVF_CUDA(cudaEventCreateWithFlags(ev, cudaEventDefault));
+    return KVF_OK;
+}
+
+void recycle_event(kvf_engine* e, cudaEvent_t ev) {
+    if (ev) e->event_pool.push_back(ev);
+}
+
+}  // namespace kvf_impl
+
+// =====================================================================================
+// kernels
+// =====================================================================================
+namespace {
+
+constexpr uint32_t kMaxPieces = 48;
+
+// One launch copies up to kMaxPieces pieces x all planes.  The work is cut into
+// fixed-size tiles (a tile never spans two plane segments) that CTAs take grid-stride.
+struct CopyParams {
+    const char* src;
+    char* dst;
+    uint64_t src_stride;  // bytes between planes in the source pool
+    uint64_t dst_stride;
+    uint64_t total_tiles;
+    uint32_t planes;
+    uint32_t npieces;
+    uint32_t tile_bytes;
+    uint32_t pad;
+    uint64_t src_off[kMaxPieces];
+    uint64_t dst_off[kMaxPieces];
+    uint64_t seg[kMaxPieces];             // bytes of the piece in one plane
+    uint64_t tile_begin[kMaxPieces + 1];  // prefix over pieces of planes*ceil(seg/tile)
+};
+
+struct TileRef {
+    const char* s;
+    char* d;
+    uint32_t len;
+};
+
+__device__ __forceinline__ TileRef locate(const CopyParams& p, uint64_t t) {
+    uint32_t lo = 0, hi = p.npieces - 1;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi + 1) >> 1;
+        if (p.tile_begin[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const uint64_t local = t - p.tile_begin[lo];
+    const uint64_t seg = p.seg[lo];
+    const uint64_t tps = (seg + p.tile_bytes - 1) / p.tile_bytes;
+    const uint64_t plane = local / tps;
+    const uint64_t off = (local - plane * tps) * p.tile_bytes;
+    TileRef r;
+    r.s = p.src + plane * p.src_stride + p.src_off[lo] + off;
+    r.d = p.dst + plane * p.dst_stride + p.dst_off[lo] + off;
+    r.len = static_cast<uint32_t>((seg - off < p.tile_bytes ? seg - off : (uint64_t)p.tile_bytes));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* ptr) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(ptr));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint4* ptr, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2* ptr) {
+    uint2 v;
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(ptr));
+    return v;
+}
+__device__ __forceinline__ void st_stream(uint2* ptr, const uint2& v) {
+    asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1,%2};" ::"l"(ptr), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// K1/K2/K3, SM vector path: every thread keeps UNROLL independent 16-B loads in flight
+// before its stores (PCIe latency hiding for K1; HBM streaming for K3).
+template <typename V, int UNROLL>
+__global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant__ CopyParams p) {
+    for (uint64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        const TileRef r = locate(p, t);
+        const V* s = reinterpret_cast<const V*>(r.s);
+        V* d = reinterpret_cast<V*>(r.d);
+        const uint32_t nvec = r.len / sizeof(V);
+        for (uint32_t base = threadIdx.x; base < nvec; base += blockDim.x * UNROLL) {
+            V v[UNROLL];
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t i = base + u * blockDim.x;
+                if (i < nvec) v[u] = ld_stream(s + i);
+            }
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint32_t i = base + u * blockDim.x;
+                if (i < nvec) st_stream(d + i, v[u]);
+            }
+        }
+    }
+}
+
+// ---- K1/K2 bulk path: the TMA bulk-copy engine moves CHUNK-byte pieces global->smem
+// (mbarrier complete_tx) and smem->global (bulk_group), one elected thread per CTA driving
+// a STAGES-deep ring, so the SM issues a handful of instructions per 16 KiB.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+struct ChunkIter {
+    uint64_t t;
+    uint32_t off;
+    TileRef cur;
+    bool valid;
+};
+
+__device__ __forceinline__ void iter_begin(const CopyParams& p, ChunkIter& it) {
+    it.t = blockIdx.x;
+    it.off = 0;
+    it.valid = it.t < p.total_tiles;
+    if (it.valid) it.cur = locate(p, it.t);
+}
+__device__ __forceinline__ void iter_next(const CopyParams& p, ChunkIter& it, uint32_t chunk) {
+    it.off += chunk;
+    if (it.off >= it.cur.len) {
+        it.t += gridDim.x;
+        it.off = 0;
+        it.valid = it.t < p.total_tiles;
+        if (it.valid) it.cur = locate(p, it.t);
+    }
+}
+
+template <int STAGES, int CHUNK>
+__global__ void __launch_bounds__(32) kvf_copy_bulk_kernel(const __grid_constant__ CopyParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar[STAGES];
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < STAGES; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    ChunkIter ld, st;
+    iter_begin(p, ld);
+    iter_begin(p, st);
+    uint32_t issued = 0;
+    auto issue_load = [&](uint32_t k) {
+        const uint32_t s = k % STAGES;
+        const uint32_t bytes = (ld.cur.len - ld.off < (uint32_t)CHUNK ? ld.cur.len - ld.off : (uint32_t)CHUNK);
+        const uint32_t b = smem_u32(&bar[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(smem + s * CHUNK)),
+            "l"(ld.cur.s + ld.off), "r"(bytes), "r"(b)
+            : "memory");
+        iter_next(p, ld, CHUNK);
+    };
+    while (ld.valid && issued < STAGES) issue_load(issued++);
+    for (uint32_t k = 0; st.valid; ++k) {
+        const uint32_t s = k % STAGES;
+        const uint32_t parity = (k / STAGES) & 1;
+        const uint32_t b = smem_u32(&bar[s]);
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                : "=r"(done)
+                : "r"(b), "r"(parity)
+                : "memory");
+        }
+        const uint32_t bytes = (st.cur.len - st.off < (uint32_t)CHUNK ? st.cur.len - st.off : (uint32_t)CHUNK);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(st.cur.d + st.off),
+                     "r"(smem_u32(smem + s * CHUNK)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        iter_next(p, st, CHUNK);
+        if (ld.valid) {
+            // stage s is reused by the next load: its store must have finished reading smem
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            issue_load(issued++);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr int kBulkStages = 8;
+constexpr int kBulkChunk = 16384;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+// Prefill emulation: the bf16 payload of token k is a pure function of its content id
+// (prefix hash), plane and global head.  One thread per 8-B word.
+__global__ void kvf_fill_kernel(char* pool, uint64_t plane_stride, uint32_t tpb, uint32_t planes, uint32_t wph,
+                                uint32_t head_offset, const uint64_t* __restrict__ slots,
+                                const uint64_t* __restrict__ cids, uint64_t ntok) {
+    const uint32_t wpt = tpb / 8;
+    const uint64_t total = static_cast<uint64_t>(planes) * ntok * wpt;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t per_plane = ntok * wpt;
+        const uint32_t plane = static_cast<uint32_t>(w / per_plane);
+        const uint64_t r = w - plane * per_plane;
+        const uint64_t k = r / wpt;
+        const uint32_t j = static_cast<uint32_t>(r - k * wpt);
+        const uint32_t h = j / wph, wi = j - h * wph;
+        const uint64_t base =
+            mix64(cids[k] ^ (static_cast<uint64_t>(plane) * 0x100000001b3ULL) ^ (static_cast<uint64_t>(head_offset + h) << 48));
+        const uint64_t val = mix64(base + wi) & 0xBFFFBFFFBFFFBFFFULL;
+        *reinterpret_cast<uint64_t*>(pool + plane * plane_stride + slots[k] * tpb + j * 8ull) = val;
+    }
+}
+
+__global__ void kvf_checksum_kernel(const char* pool, uint64_t plane_stride, uint32_t tpb, uint32_t planes,
+                                    const uint64_t* __restrict__ slots, uint64_t ntok, unsigned long long* out) {
+    const uint32_t wpt = tpb / 8;
+    const uint64_t total = static_cast<uint64_t>(planes) * ntok * wpt;
+    uint64_t acc = 0;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t per_plane = ntok * wpt;
+        const uint32_t plane = static_cast<uint32_t>(w / per_plane);
+        const uint64_t r = w - plane * per_plane;
+        const uint64_t k = r / wpt;
+        const uint32_t j = static_cast<uint32_t>(r - k * wpt);
+        const uint64_t word = *reinterpret_cast<const uint64_t*>(pool + plane * plane_stride + slots[k] * tpb + j * 8ull);
+        acc += mix64(word ^ (w * 0x9e3779b97f4a7c15ULL));
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(acc));
+}
+
+}  // namespace
+
+// =====================================================================================
+// engine internals
+// =====================================================================================
+namespace {
+
+char* tier_base(kvf_engine* e, int tier) { return tier == KVF_TIER_DEVICE ? e->dev_pool : e->host_pool_dev; }
+uint64_t tier_slots(const kvf_engine* e, int tier) { return tier == KVF_TIER_DEVICE ? e->dev_slots : e->host_slots; }
+
+bool runs_valid(const kvf_engine* e, int tier, const kvf_run* runs, uint32_t n, uint64_t* total) {
+    uint64_t cap = tier_slots(e, tier), t = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        if (runs[i].start + runs[i].len > cap || runs[i].start + runs[i].len < runs[i].start) return false;
+        t += runs[i].len;
+    }
+    *total = t;
+    return true;
+}
+
+struct Endpoint {
+    const char* base;
+    uint64_t stride;  // bytes between planes
+    bool host;
+};
+
+// Launch the copy of `pieces` (all planes) between two pools on `stream`.
+int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const Endpoint& dst,
+                const std::vector<Piece>& pieces, uint32_t mode, uint32_t ctas) {
+    const uint64_t tpb = e->tpb;
+    for (size_t first = 0; first < pieces.size(); first += kMaxPieces) {
+        const uint32_t np = static_cast<uint32_t>(std::min<size_t>(kMaxPieces, pieces.size() - first));
+        if (mode == KVF_COPY_CE) {
+            for (uint32_t i = 0; i < np; ++i) {
+                const Piece& pc = pieces[first + i];
+                KVF_CUDA(cudaMemcpy2DAsync(const_cast<char*>(dst.base) + pc.dst_slot * tpb, dst.stride,
+                                           src.base + pc.src_slot * tpb, src.stride, pc.ntok * tpb, e->planes,
+                                           cudaMemcpyDefault, stream));
+            }
+            continue;
+        }
+        CopyParams p;
+        std::memset(&p, 0, sizeof(p));
+        p.src = src.base;
+        p.dst = const_cast<char*>(dst.base);
+        p.src_stride = src.stride;
+        p.dst_stride = dst.stride;
+        p.planes = e->planes;
+        p.npieces = np;
+        const bool vec16 = (tpb % 16) == 0;
+        uint32_t threads = 512, unroll = 8;
+        p.tile_bytes = threads * unroll * (vec16 ? 16 : 8);  // 64 KiB (16-B vectors)
+        uint64_t tiles = 0;
+        for (uint32_t i = 0; i < np; ++i) {
+            const Piece& pc = pieces[first + i];
+            p.src_off[i] = pc.src_slot * tpb;
+            p.dst_off[i] = pc.dst_slot * tpb;
+            p.seg[i] = pc.ntok * tpb;
+            p.tile_begin[i] = tiles;
+            tiles += static_cast<uint64_t>(e->planes) * ((p.seg[i] + p.tile_bytes - 1) / p.tile_bytes);
+        }
+        p.tile_begin[np] = tiles;
+        p.total_tiles = tiles;
+        if (tiles == 0) continue;
+        uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(ctas, tiles));
+        if (mode == KVF_COPY_SM_BULK && vec16) {
+            const size_t smem = static_cast<size_t>(kBulkStages) * kBulkChunk;
+            static bool attr_set = false;
+            if (!attr_set) {
+                KVF_CUDA(cudaFuncSetAttribute(kvf_copy_bulk_kernel<kBulkStages, kBulkChunk>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                attr_set = true;
+            }
+            kvf_copy_bulk_kernel<kBulkStages, kBulkChunk><<<grid, 32, smem, stream>>>(p);
+        } else if (vec16) {
+            kvf_copy_vec_kernel<uint4, 8><<<grid, threads, 0, stream>>>(p);
+        } else {
+            kvf_copy_vec_kernel<uint2, 8><<<grid, threads, 0, stream>>>(p);
+        }
+        KVF_CUDA(cudaGetLastError());
+        e->stats.kernel_launches++;
+    }
+    return KVF_OK;
+}
+
+int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j) {
+    if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
+    int rc = acquire_event(e, &j.start);
+    if (rc) return rc;
+    rc = acquire_event(e, &j.stop);
+    if (rc) return rc;
+    j.stream = stream;
+    KVF_CUDA(cudaEventRecord(j.start, stream));
+    return KVF_OK;
+}
+
+int end_job(kvf_engine* e, uint64_t job_id, Job& j) {
+    KVF_CUDA(cudaEventRecord(j.stop, j.stream));
+    e->jobs.emplace(job_id, j);
+    return KVF_OK;
+}
+
+int transfer(kvf_engine* e, uint64_t job_id, int src_tier, const kvf_run* src_runs, uint32_t n_src, int dst_tier,
+             const kvf_run* dst_runs, uint32_t n_dst) {
+    uint64_t ts = 0, td = 0;
+    if ((n_src && !src_runs) || (n_dst && !dst_runs)) return set_error(KVF_E_INVALID_ARG, "null run list");
+    if (!runs_valid(e, src_tier, src_runs, n_src, &ts) || !runs_valid(e, dst_tier, dst_runs, n_dst, &td))
+        return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    if (ts != td) return set_error(KVF_E_INVALID_ARG, "source and destination token counts differ");
+    std::vector<Piece> pieces;
+    merge_runs(src_runs, n_src, dst_runs, n_dst, pieces);
+    const bool h2d = src_tier == KVF_TIER_HOST && dst_tier == KVF_TIER_DEVICE;
+    const bool d2h = src_tier == KVF_TIER_DEVICE && dst_tier == KVF_TIER_HOST;
+    cudaStream_t st = h2d ? e->s_h2d : (d2h ? e->s_d2h : e->s_dev);
+    Job j;
+    int rc = begin_job(e, job_id, st, j);
+    if (rc) return rc;
+    if (d2h && e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(st, e->dev_write_done, 0));
+    const uint64_t stride_s = tier_slots(e, src_tier) * e->tpb, stride_d = tier_slots(e, dst_tier) * e->tpb;
+    Endpoint src{tier_base(e, src_tier), stride_s, src_tier == KVF_TIER_HOST};
+    Endpoint dst{tier_base(e, dst_tier), stride_d, dst_tier == KVF_TIER_HOST};
+    const bool pcie = h2d || d2h;
+    const uint32_t mode = pcie ? e->cfg.pcie_mode : KVF_COPY_SM_VEC;
+    const uint32_t ctas = pcie ? e->cfg.pcie_ctas : e->cfg.hbm_ctas;
+    rc = launch_copy(e, st, src, dst, pieces, mode, ctas);
+    if (rc) return rc;
+    j.bytes = ts * e->token_bytes;
+    if (h2d) { e->stats.h2d_bytes += j.bytes; e->stats.h2d_jobs++; }
+    else if (d2h) { e->stats.d2h_bytes += j.bytes; e->stats.d2h_jobs++; }
+    else { e->stats.dev_bytes += j.bytes; e->stats.dev_jobs++; }
+    return end_job(e, job_id, j);
+}
+
+// K3 between the pool and a contiguous staging buffer (a 1-run pool of ntok slots).
+int dev_staging_copy(kvf_engine* e, uint64_t job_id, const kvf_run* runs, uint32_t n, char* staging, bool gather) {
+    uint64_t ntok = 0;
+    if (!staging) return set_error(KVF_E_INVALID_ARG, "null staging buffer");
+    if (!runs_valid(e, KVF_TIER_DEVICE, runs, n, &ntok)) return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    kvf_run whole{0, ntok};
+    std::vector<Piece> pieces;
+    if (gather) merge_runs(runs, n, &whole, 1, pieces);
+    else merge_runs(&whole, 1, runs, n, pieces);
+    Job j;
+    int rc = begin_job(e, job_id, e->s_dev, j);
+    if (rc) return rc;
+    Endpoint pool{e->dev_pool, e->dev_slots * e->tpb, false};
+    Endpoint stage{staging, ntok * e->tpb, false};
+    rc = gather ? launch_copy(e, e->s_dev, pool, stage, pieces, KVF_COPY_SM_VEC, e->cfg.hbm_ctas)
+                : launch_copy(e, e->s_dev, stage, pool, pieces, KVF_COPY_SM_VEC, e->cfg.hbm_ctas);
+    if (rc) return rc;
+    if (!gather) {
+        KVF_CUDA(cudaEventRecord(e->dev_write_done, e->s_dev));
+        e->dev_write_pending = true;
+    }
+    j.bytes = ntok * e->token_bytes;
+    e->stats.dev_bytes += j.bytes;
+    e->stats.dev_jobs++;
+    return end_job(e, job_id, j);
+}
+
+// Upload (slot, cid) per token into the dev workspace; returns device pointers.
+int stage_slots(kvf_engine* e, const kvf_run* runs, uint32_t n, const uint64_t* cids, uint64_t ntok,
+                uint64_t** d_slots, uint64_t** d_cids) {
+    const size_t bytes = ntok * sizeof(uint64_t) * (cids ? 2 : 1);
+    // the dev workspace may still be read by an in-flight fill: drain s_dev first
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    int rc = e->ws_dev.ensure(bytes + 64, bytes + 64);
+    if (rc) return rc;
+    uint64_t* h = static_cast<uint64_t*>(e->ws_dev.host);
+    uint64_t k = 0;
+    for (uint32_t r = 0; r < n; ++r)
+        for (uint64_t t = 0; t < runs[r].len; ++t) h[k++] = runs[r].start + t;
+    if (cids) std::memcpy(h + ntok, cids, ntok * sizeof(uint64_t));
+    KVF_CUDA(cudaMemcpyAsync(e->ws_dev.dev, h, bytes, cudaMemcpyHostToDevice, e->s_dev));
+    *d_slots = static_cast<uint64_t*>(e->ws_dev.dev);
+    if (d_cids) *d_cids = cids ? static_cast<uint64_t*>(e->ws_dev.dev) + ntok : nullptr;
+    return KVF_OK;
+}
+
+uint32_t grid_for(const kvf_engine* e, uint64_t work, uint32_t threads) {
+    uint64_t g = (work + threads - 1) / threads;
+    return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(g, static_cast<uint64_t>(e->sm_count) * 8)));
+}
+
+}  // namespace
+
+// =====================================================================================
+// C-ABI
+// =====================================================================================
+#define KVF_GUARD(e) \
+    if (!(e)) return set_error(KVF_E_INVALID_ARG, "null engine"); \
+    std::lock_guard<std::mutex> _lk((e)->mu); \
+    if (cudaSetDevice((e)->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed")
+
+extern "C" {
+
+const char* kvf_last_error(void) { return g_last_error.c_str(); }
+const char* kvf_version(void) { return "kvflow-b200 0.1 (sm_100a)"; }
+
+int kvf_device_count(int32_t* out) {
+    int n = 0;
+    cudaError_t err = cudaGetDeviceCount(&n);
+    if (err != cudaSuccess) n = 0;
+    if (out) *out = n;
+    return KVF_OK;
+}
+
+int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_engine** out) {
+    if (!g || !cfg || !out) return set_error(KVF_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (g->layers == 0 || g->kv_heads_local == 0 || g->head_dim == 0 || g->dtype_bytes != 2 ||
+        g->head_offset + g->kv_heads_local > g->kv_heads_total)
+        return set_error(KVF_E_CONFIG, "invalid geometry (bf16 only; heads within total)");
+    if ((static_cast<uint64_t>(g->kv_heads_local) * g->head_dim * g->dtype_bytes) % 8 != 0)
+        return set_error(KVF_E_CONFIG, "bytes per token per plane must be a multiple of 8");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_error(KVF_E_NO_DEVICE, "no CUDA device: kvflow has no CPU fallback");
+    if (cfg->device < 0 || cfg->device >= ndev) return set_error(KVF_E_INVALID_ARG, "device ordinal out of range");
+    auto* e = new kvf_engine();
+    e->geom = *g;
+    e->cfg = *cfg;
+    e->device = cfg->device;
+    e->tpb = static_cast<uint64_t>(g->kv_heads_local) * g->head_dim * g->dtype_bytes;
+    e->planes = g->layers * 2;
+    e->token_bytes = e->tpb * e->planes;
+    auto fail = [&](int rc) {
+        kvf_engine_destroy(e);
+        return rc;
+    };
+    if (cudaSetDevice(e->device) != cudaSuccess) return fail(set_error(KVF_E_CUDA, "cudaSetDevice"));
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->sm_count = prop.multiProcessorCount;
+    if (e->cfg.pcie_ctas == 0) e->cfg.pcie_ctas = 32;
+    if (e->cfg.hbm_ctas == 0) e->cfg.hbm_ctas = static_cast<uint32_t>(e->sm_count) * 4;
+    cudaError_t err;
+    e->dev_slots = cfg->gpu_slots;
+    e->host_slots = cfg->host_slots;
+    if (e->dev_slots) {
+        err = cudaMalloc(reinterpret_cast<void**>(&e->dev_pool), e->dev_slots * e->token_bytes);
+        if (err != cudaSuccess) return fail(cuda_error(err, "cudaMalloc(device KV pool)"));
+    }
+    if (e->host_slots) {
+        const size_t bytes = e->host_slots * e->token_bytes;
+        if (cfg->host_numa_node >= 0) {
+            // NUMA-local pinned shard: mmap, bind to the GPU's node, then pin + map.
+            void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+            if (p == MAP_FAILED) return fail(set_error(KVF_E_OUT_OF_HOST_SLOTS, "mmap host pool"));
+            unsigned long mask[16] = {0};
+            const int node = cfg->host_numa_node;
+            if (node < 1024) mask[node / 64] |= 1ul << (node % 64);
+            syscall(SYS_mbind, p, bytes, 2 /*MPOL_BIND*/, mask, 1024ul, 0u);  // best effort
+            e->host_pool = static_cast<char*>(p);
+            e->host_map_bytes = bytes;
+            err = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+            if (err != cudaSuccess) return fail(cuda_error(err, "cudaHostRegister(host KV pool)"));
+            e->host_registered = true;
+        } else {
+            err = cudaHostAlloc(reinterpret_cast<void**>(&e->host_pool), bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+            if (err != cudaSuccess) return fail(cuda_error(err, "cudaHostAlloc(host KV pool)"));
+        }
+        void* dp = nullptr;
+        err = cudaHostGetDevicePointer(&dp, e->host_pool, 0);
+        if (err != cudaSuccess) return fail(cuda_error(err, "cudaHostGetDevicePointer"));
+        e->host_pool_dev = static_cast<char*>(dp);
+    }
+    e->alloc[KVF_TIER_DEVICE].reset(e->dev_slots);
+    e->alloc[KVF_TIER_HOST].reset(e->host_slots);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if ((err = cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->s_dev, cudaStreamNonBlocking)) != cudaSuccess ||
+        (err = cudaStreamCreateWithPriority(&e->s_dec, cudaStreamNonBlocking, hi)) != cudaSuccess)
+        return fail(cuda_error(err, "cudaStreamCreate"));
+    if ((err = cudaEventCreateWithFlags(&e->dev_write_done, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(cuda_error(err, "cudaEventCreate"));
+    if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_checksum), sizeof(uint64_t))) != cudaSuccess)
+        return fail(cuda_error(err, "cudaMalloc(checksum)"));
+    *out = e;
+    return KVF_OK;
+}
+
+int kvf_engine_destroy(kvf_engine* e) {
+    if (!e) return KVF_OK;
+    cudaSetDevice(e->device);
+    cudaDeviceSynchronize();
+    for (auto& [id, j] : e->jobs) {
+        cudaEventDestroy(j.start);
+        cudaEventDestroy(j.stop);
+    }
+    for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
+    if (e->dev_write_done) cudaEventDestroy(e->dev_write_done);
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec})
+        if (s) cudaStreamDestroy(s);
+    e->ws_dev.release();
+    e->ws_dec.release();
+    if (e->d_checksum) cudaFree(e->d_checksum);
+    if (e->dev_pool) cudaFree(e->dev_pool);
+    if (e->host_pool) {
+        if (e->host_registered) {
+            cudaHostUnregister(e->host_pool);
+            munmap(e->host_pool, e->host_map_bytes);
+        } else {
+            cudaFreeHost(e->host_pool);
+        }
+    }
+    delete e;
+    return KVF_OK;
+}
+
+int kvf_engine_token_bytes(const kvf_engine* e, uint64_t* tpb, uint64_t* token_bytes) {
+    if (!e) return set_error(KVF_E_INVALID_ARG, "null engine");
+    if (tpb) *tpb = e->tpb;
+    if (token_bytes) *token_bytes = e->token_bytes;
+    return KVF_OK;
+}
+
+int kvf_engine_set_copy_mode(kvf_engine* e, uint32_t mode, uint32_t pcie_ctas, uint32_t hbm_ctas) {
+    KVF_GUARD(e);
+    if (mode > KVF_COPY_CE) return set_error(KVF_E_INVALID_ARG, "unknown copy mode");
+    e->cfg.pcie_mode = mode;
+    if (pcie_ctas) e->cfg.pcie_ctas = pcie_ctas;
+    if (hbm_ctas) e->cfg.hbm_ctas = hbm_ctas;
+    return KVF_OK;
+}
+
+int kvf_slots_alloc(kvf_engine* e, int32_t tier, uint64_t tokens, kvf_run* out, uint32_t max_runs, uint32_t* n_runs) {
+    if (!e || !out || !n_runs || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    std::lock_guard<std::mutex> lk(e->mu);
+    std::vector<kvf_run> runs;
+    if (!e->alloc[tier].alloc(tokens, runs))
+        return set_error(tier == KVF_TIER_DEVICE ? KVF_E_OUT_OF_GPU_MEMORY : KVF_E_OUT_OF_HOST_SLOTS,
+                         "slot pool exhausted: want " + std::to_string(tokens) + " tokens, free " +
+                             std::to_string(e->alloc[tier].free_tokens()));
+    if (runs.size() > max_runs) {
+        for (const kvf_run& r : runs) e->alloc[tier].release(r);
+        return set_error(KVF_E_TOO_LARGE, "allocation needs " + std::to_string(runs.size()) + " runs > max_runs");
+    }
+    std::copy(runs.begin(), runs.end(), out);
+    *n_runs = static_cast<uint32_t>(runs.size());
+    return KVF_OK;
+}
+
+int kvf_slots_free(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n) {
+    if (!e || (n && !runs) || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    std::lock_guard<std::mutex> lk(e->mu);
+    for (uint32_t i = 0; i < n; ++i)
+        if (!e->alloc[tier].release(runs[i]))
+            return set_error(KVF_E_INTERNAL, "slot free of an unallocated or out-of-range run");
+    return KVF_OK;
+}
+
+int kvf_slots_free_count(const kvf_engine* e, int32_t tier, uint64_t* free_tokens, uint64_t* free_runs) {
+    if (!e || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    if (free_tokens) *free_tokens = e->alloc[tier].free_tokens();
+    if (free_runs) *free_runs = e->alloc[tier].free_runs();
+    return KVF_OK;
+}
+
+int kvf_pool_ptr(const kvf_engine* e, int32_t tier, void** base, uint64_t* slots) {
+    if (!e || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    if (base) *base = tier == KVF_TIER_DEVICE ? static_cast<void*>(e->dev_pool) : static_cast<void*>(e->host_pool);
+    if (slots) *slots = tier == KVF_TIER_DEVICE ? e->dev_slots : e->host_slots;
+    return KVF_OK;
+}
+
+int kvf_h2d_gather(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host, const kvf_run* dev_runs,
+                   uint32_t n_dev) {
+    KVF_GUARD(e);
+    return transfer(e, job_id, KVF_TIER_HOST, host_runs, n_host, KVF_TIER_DEVICE, dev_runs, n_dev);
+}
+
+int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint32_t n_dev, const kvf_run* host_runs,
+                    uint32_t n_host) {
+    KVF_GUARD(e);
+    return transfer(e, job_id, KVF_TIER_DEVICE, dev_runs, n_dev, KVF_TIER_HOST, host_runs, n_host);
+}
+
+int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* runs, uint32_t n, void* staging) {
+    KVF_GUARD(e);
+    return dev_staging_copy(e, job_id, runs, n, static_cast<char*>(staging), true);
+}
+
+int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* runs, uint32_t n) {
+    KVF_GUARD(e);
+    return dev_staging_copy(e, job_id, runs, n, static_cast<char*>(const_cast<void*>(staging)), false);
+}
+
+int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    cudaError_t err = cudaEventQuery(it->second.stop);
+    if (err == cudaErrorNotReady) {
+        *done = 0;
+        return KVF_OK;
+    }
+    if (err != cudaSuccess) return cuda_error(err, "cudaEventQuery(job)");
+    *done = 1;
+    return KVF_OK;
+}
+
+int kvf_job_wait(kvf_engine* e, uint64_t job_id) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    KVF_CUDA(cudaEventSynchronize(it->second.stop));
+    return KVF_OK;
+}
+
+int kvf_job_elapsed_ms(kvf_engine* e, uint64_t job_id, float* ms) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    KVF_CUDA(cudaEventSynchronize(it->second.stop));
+    KVF_CUDA(cudaEventElapsedTime(ms, it->second.start, it->second.stop));
+    return KVF_OK;
+}
+
+int kvf_job_release(kvf_engine* e, uint64_t job_id) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    KVF_CUDA(cudaEventSynchronize(it->second.stop));
+    recycle_event(e, it->second.start);
+    recycle_event(e, it->second.stop);
+    e->jobs.erase(it);
+    return KVF_OK;
+}
+
+int kvf_sync_all(kvf_engine* e) {
+    KVF_GUARD(e);
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec}) KVF_CUDA(cudaStreamSynchronize(s));
+    return KVF_OK;
+}
+
+int kvf_fill_payload(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n, const uint64_t* cids, uint64_t ntok) {
+    KVF_GUARD(e);
+    if (tier != 0 && tier != 1) return set_error(KVF_E_INVALID_ARG, "bad tier");
+    uint64_t total = 0;
+    if (!runs_valid(e, tier, runs, n, &total) || total != ntok || (ntok && !cids))
+        return set_error(KVF_E_INVALID_ARG, "fill: runs/cids mismatch");
+    if (ntok == 0) return KVF_OK;
+    uint64_t *d_slots = nullptr, *d_cids = nullptr;
+    int rc = stage_slots(e, runs, n, cids, ntok, &d_slots, &d_cids);
+    if (rc) return rc;
+    const uint64_t words = static_cast<uint64_t>(e->planes) * ntok * (e->tpb / 8);
+    kvf_fill_kernel<<<grid_for(e, words, 256), 256, 0, e->s_dev>>>(
+        tier_base(e, tier), tier_slots(e, tier) * e->tpb, static_cast<uint32_t>(e->tpb), e->planes,
+        e->geom.head_dim / 4, e->geom.head_offset, d_slots, d_cids, ntok);
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    KVF_CUDA(cudaEventRecord(e->dev_write_done, e->s_dev));
+    e->dev_write_pending = true;
+    return KVF_OK;
+}
+
+int kvf_checksum(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n, uint64_t* out) {
+    KVF_GUARD(e);
+    if (!out || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    uint64_t ntok = 0;
+    if (!runs_valid(e, tier, runs, n, &ntok)) return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    // make every outstanding transfer visible first (a checksum is a verification read)
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h}) KVF_CUDA(cudaStreamSynchronize(s));
+    *out = 0;
+    if (ntok == 0) return KVF_OK;
+    uint64_t* d_slots = nullptr;
+    int rc = stage_slots(e, runs, n, nullptr, ntok, &d_slots, nullptr);
+    if (rc) return rc;
+    KVF_CUDA(cudaMemsetAsync(e->d_checksum, 0, sizeof(uint64_t), e->s_dev));
+    const uint64_t words = static_cast<uint64_t>(e->planes) * ntok * (e->tpb / 8);
+    kvf_checksum_kernel<<<grid_for(e, words, 256), 256, 0, e->s_dev>>>(
+        tier_base(e, tier), tier_slots(e, tier) * e->tpb, static_cast<uint32_t>(e->tpb), e->planes, d_slots, ntok,
+        reinterpret_cast<unsigned long long*>(e->d_checksum));
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    KVF_CUDA(cudaMemcpyAsync(out, e->d_checksum, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s_dev));
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    return KVF_OK;
+}
+
+int kvf_read_runs(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n, void* dst, uint64_t dst_bytes) {
+    KVF_GUARD(e);
+    if (!dst || (tier != 0 && tier != 1)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    uint64_t ntok = 0;
+    if (!runs_valid(e, tier, runs, n, &ntok)) return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    if (dst_bytes < ntok * e->token_bytes) return set_error(KVF_E_INVALID_ARG, "destination too small");
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h}) KVF_CUDA(cudaStreamSynchronize(s));
+    if (ntok == 0) return KVF_OK;
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    const size_t bytes = ntok * e->token_bytes;
+    int rc = e->ws_dev.ensure(bytes, 64);
+    if (rc) return rc;
+    kvf_run whole{0, ntok};
+    std::vector<Piece> pieces;
+    merge_runs(runs, n, &whole, 1, pieces);
+    Endpoint src{tier_base(e, tier), tier_slots(e, tier) * e->tpb, tier == KVF_TIER_HOST};
+    Endpoint dstp{static_cast<char*>(e->ws_dev.dev), ntok * e->tpb, false};
+    rc = launch_copy(e, e->s_dev, src, dstp, pieces, KVF_COPY_SM_VEC, e->cfg.hbm_ctas);
+    if (rc) return rc;
+    KVF_CUDA(cudaMemcpyAsync(dst, e->ws_dev.dev, bytes, cudaMemcpyDeviceToHost, e->s_dev));
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    return KVF_OK;
+}
+
+int kvf_get_stats(const kvf_engine* e, kvf_stats* out) {
+    if (!e || !out) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    *out = e->stats;
+    return KVF_OK;
+}
+
+}  // extern "C"

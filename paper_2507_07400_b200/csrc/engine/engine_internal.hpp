@@ -1,0 +1,109 @@
+// Internal declarations shared by the translation units of libkvflow.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kvflow.h"
+
+namespace kvf_impl {
+
+// ---- error plumbing: thread-local last error, int status everywhere -------------------
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* what);
+
+#define KVF_CUDA(call)                                       \
+    do {                                                     \
+        cudaError_t _e = (call);                             \
+        if (_e != cudaSuccess) return cuda_error(_e, #call); \
+    } while (0)
+
+// ---- token-slot allocator: free intervals with a size index ----------------------------
+class SlotAllocator {
+public:
+    void reset(uint64_t slots);
+    // best-fit single run, else largest-first multi-run; false if not enough free slots
+    bool alloc(uint64_t tokens, std::vector<kvf_run>& out);
+    // returns false on double free / out of range
+    bool release(const kvf_run& r);
+    uint64_t free_tokens() const { return free_tokens_; }
+    uint64_t free_runs() const { return by_start_.size(); }
+    uint64_t capacity() const { return capacity_; }
+
+private:
+    void insert_free(uint64_t start, uint64_t len);
+    void erase_free(std::map<uint64_t, uint64_t>::iterator it);
+    std::map<uint64_t, uint64_t> by_start_;           // start -> len
+    std::multimap<uint64_t, uint64_t> by_len_;        // len -> start
+    uint64_t capacity_ = 0;
+    uint64_t free_tokens_ = 0;
+};
+
+// ---- copy descriptors ---------------------------------------------------------------
+// A piece is a token range contiguous in both source and destination pools.
+struct Piece {
+    uint64_t src_slot, dst_slot, ntok;
+};
+void merge_runs(const kvf_run* a, uint32_t na, const kvf_run* b, uint32_t nb, std::vector<Piece>& out);
+
+struct Job {
+    cudaEvent_t start = nullptr, stop = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t bytes = 0;
+};
+
+struct Workspace {  // grow-only device + pinned staging buffers
+    void* dev = nullptr;
+    size_t dev_bytes = 0;
+    void* host = nullptr;
+    size_t host_bytes = 0;
+    int ensure(size_t dev_need, size_t host_need);
+    void release();
+};
+
+}  // namespace kvf_impl
+
+struct kvf_engine {
+    kvf_geometry geom{};
+    kvf_engine_config cfg{};
+    int device = 0;
+    int sm_count = 148;
+    uint64_t tpb = 0;          // bytes per token per plane on this shard
+    uint32_t planes = 0;       // layers * 2
+    uint64_t token_bytes = 0;  // tpb * planes
+
+    char* dev_pool = nullptr;
+    uint64_t dev_slots = 0;
+    char* host_pool = nullptr;      // host address
+    char* host_pool_dev = nullptr;  // device-side address of the same memory
+    uint64_t host_slots = 0;
+    bool host_registered = false;   // mmap+cudaHostRegister (NUMA-bound) vs cudaHostAlloc
+    size_t host_map_bytes = 0;
+
+    kvf_impl::SlotAllocator alloc[2];
+
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_dev = nullptr, s_dec = nullptr;
+    cudaEvent_t dev_write_done = nullptr;  // last fill / K3 scatter on s_dev
+    bool dev_write_pending = false;
+
+    std::unordered_map<uint64_t, kvf_impl::Job> jobs;
+    std::vector<cudaEvent_t> event_pool;
+
+    kvf_impl::Workspace ws_dev;  // fill / checksum / read staging (s_dev)
+    kvf_impl::Workspace ws_dec;  // decision kernels (s_dec)
+
+    uint64_t* d_checksum = nullptr;
+    kvf_stats stats{};
+    std::mutex mu;  // engine calls are serialised per engine
+};
+
+namespace kvf_impl {
+int acquire_event(kvf_engine* e, cudaEvent_t* ev);
+void recycle_event(kvf_engine* e, cudaEvent_t ev);
+}  // namespace kvf_impl

@@ -1,0 +1,201 @@
+"""Thin Python handle over the libkvflow.so C-ABI (include/kvflow.h).
+
+Used by tests, smoke() and bench.py to drive the CUDA engine directly.  The
+reference-facing cache-manager API (RadixCache / TierManager / Simulator) is the C++
+control plane in include/kvflow/*.hpp; this module is only plumbing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+def device_count() -> int:
+    n = C.c_int32()
+    N.engine_lib().kvf_device_count(C.byref(n))
+    return n.value
+
+
+class Engine:
+    """One KV-movement engine = one GPU shard (HBM pool + pinned host pool + streams)."""
+
+    def __init__(self, layers=32, kv_heads_total=8, kv_heads_local=None, head_offset=0, head_dim=128,
+                 gpu_slots=0, host_slots=0, device=0, pcie_mode=N.KVF_COPY_SM_VEC, pcie_ctas=0, hbm_ctas=0,
+                 numa_node=-1):
+        L = N.engine_lib()
+        self._lib = L
+        g = N.Geometry(layers, kv_heads_total, kv_heads_local or kv_heads_total, head_offset, head_dim, 2)
+        cfg = N.EngineConfig(device, gpu_slots, host_slots, pcie_ctas, pcie_mode, hbm_ctas, numa_node)
+        h = C.c_void_p()
+        N.check(L.kvf_engine_create(C.byref(g), C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.geom = g
+        tpb, tb = C.c_uint64(), C.c_uint64()
+        N.check(L.kvf_engine_token_bytes(h, C.byref(tpb), C.byref(tb)))
+        self.tpb, self.token_bytes = tpb.value, tb.value
+        self.gpu_slots, self.host_slots = gpu_slots, host_slots
+        self._next_job = 1
+
+    def close(self):
+        if self.h:
+            self._lib.kvf_engine_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- pools ---------------------------------------------------------------------
+    def alloc(self, tier, tokens, max_runs=4096):
+        out = (N.Run * max_runs)()
+        n = C.c_uint32()
+        N.check(self._lib.kvf_slots_alloc(self.h, tier, tokens, out, max_runs, C.byref(n)))
+        return [(out[i].start, out[i].len) for i in range(n.value)]
+
+    def free(self, tier, runs):
+        N.check(self._lib.kvf_slots_free(self.h, tier, N.runs_array(runs), len(runs)))
+
+    def free_count(self, tier):
+        t, r = C.c_uint64(), C.c_uint64()
+        N.check(self._lib.kvf_slots_free_count(self.h, tier, C.byref(t), C.byref(r)))
+        return t.value, r.value
+
+    def pool_ptr(self, tier):
+        p, s = C.c_void_p(), C.c_uint64()
+        N.check(self._lib.kvf_pool_ptr(self.h, tier, C.byref(p), C.byref(s)))
+        return p.value, s.value
+
+    def host_pool_array(self):
+        """numpy uint8 view of the pinned host pool (for verification only)."""
+        p, s = self.pool_ptr(N.KVF_TIER_HOST)
+        buf = (C.c_uint8 * (s * self.token_bytes)).from_address(p)
+        return np.frombuffer(buf, dtype=np.uint8)
+
+    # ---- jobs ------------------------------------------------------------------------
+    def new_job(self):
+        j = self._next_job
+        self._next_job += 1
+        return j
+
+    def h2d(self, host_runs, dev_runs, job=None):
+        job = job or self.new_job()
+        N.check(self._lib.kvf_h2d_gather(self.h, job, N.runs_array(host_runs), len(host_runs),
+                                         N.runs_array(dev_runs), len(dev_runs)))
+        return job
+
+    def d2h(self, dev_runs, host_runs, job=None):
+        job = job or self.new_job()
+        N.check(self._lib.kvf_d2h_scatter(self.h, job, N.runs_array(dev_runs), len(dev_runs),
+                                          N.runs_array(host_runs), len(host_runs)))
+        return job
+
+    def dev_gather(self, dev_runs, staging_ptr, job=None):
+        job = job or self.new_job()
+        N.check(self._lib.kvf_dev_gather(self.h, job, N.runs_array(dev_runs), len(dev_runs), staging_ptr))
+        return job
+
+    def dev_scatter(self, staging_ptr, dev_runs, job=None):
+        job = job or self.new_job()
+        N.check(self._lib.kvf_dev_scatter(self.h, job, staging_ptr, N.runs_array(dev_runs), len(dev_runs)))
+        return job
+
+    def query(self, job):
+        d = C.c_int32()
+        N.check(self._lib.kvf_job_query(self.h, job, C.byref(d)))
+        return bool(d.value)
+
+    def wait(self, job):
+        N.check(self._lib.kvf_job_wait(self.h, job))
+
+    def elapsed_ms(self, job):
+        ms = C.c_float()
+        N.check(self._lib.kvf_job_elapsed_ms(self.h, job, C.byref(ms)))
+        return ms.value
+
+    def release(self, job):
+        N.check(self._lib.kvf_job_release(self.h, job))
+
+    def sync(self):
+        N.check(self._lib.kvf_sync_all(self.h))
+
+    def set_copy_mode(self, mode, pcie_ctas=0, hbm_ctas=0):
+        N.check(self._lib.kvf_engine_set_copy_mode(self.h, mode, pcie_ctas, hbm_ctas))
+
+    # ---- payload / verification -----------------------------------------------------
+    def fill(self, tier, runs, cids):
+        cids = np.ascontiguousarray(cids, dtype=np.uint64)
+        N.check(self._lib.kvf_fill_payload(self.h, tier, N.runs_array(runs), len(runs), cids.ctypes.data,
+                                           len(cids)))
+
+    def checksum(self, tier, runs):
+        out = C.c_uint64()
+        N.check(self._lib.kvf_checksum(self.h, tier, N.runs_array(runs), len(runs), C.byref(out)))
+        return out.value
+
+    def read(self, tier, runs):
+        ntok = sum(l for _, l in runs)
+        buf = np.zeros(ntok * self.token_bytes, dtype=np.uint8)
+        N.check(self._lib.kvf_read_runs(self.h, tier, N.runs_array(runs), len(runs), buf.ctypes.data, buf.nbytes))
+        return buf
+
+    def stats(self):
+        s = N.Stats()
+        N.check(self._lib.kvf_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in N.Stats._fields_}
+
+    # ---- decisions ---------------------------------------------------------------------
+    def priority(self, parent, bidx, cand):
+        parent = np.ascontiguousarray(parent, dtype=np.int32)
+        bidx = np.ascontiguousarray(bidx, dtype=np.int32)
+        cand = np.ascontiguousarray(cand, dtype=np.int64)
+        out = np.zeros(len(parent), dtype=np.int64)
+        N.check(self._lib.kvf_priority_propagate(self.h, parent.ctypes.data, len(parent), bidx.ctypes.data,
+                                                 cand.ctypes.data, len(bidx), out.ctypes.data))
+        return out
+
+    def victims(self, tree, needed, workflow_aware, offload, has_floor=False, floor=0, cpu_used=0, cpu_cap=0):
+        """tree: dict of numpy arrays parent/depth/status/lock/rank/time/seq/id/tokens/backed + bpt."""
+        arrs = {
+            "parent": np.ascontiguousarray(tree["parent"], dtype=np.int32),
+            "depth": np.ascontiguousarray(tree["depth"], dtype=np.uint16),
+            "status": np.ascontiguousarray(tree["status"], dtype=np.uint8),
+            "lock": np.ascontiguousarray(tree["lock"], dtype=np.int32),
+            "rank": np.ascontiguousarray(tree["rank"], dtype=np.int64),
+            "time": np.ascontiguousarray(tree["time"], dtype=np.float64),
+            "seq": np.ascontiguousarray(tree["seq"], dtype=np.uint64),
+            "id": np.ascontiguousarray(tree["id"], dtype=np.uint64),
+            "tokens": np.ascontiguousarray(tree["tokens"], dtype=np.uint64),
+            "backed": np.ascontiguousarray(tree["backed"], dtype=np.uint8),
+        }
+        n = len(arrs["parent"])
+        tv = N.TreeView(n, *(arrs[k].ctypes.data for k in
+                             ("parent", "depth", "status", "lock", "rank", "time", "seq", "id", "tokens", "backed")),
+                        int(tree["bpt"]))
+        req = N.EvictRequest(int(needed), int(bool(workflow_aware)), int(bool(offload)), int(bool(has_floor)),
+                             int(floor), int(cpu_used), int(cpu_cap))
+        idx = np.zeros(max(1, n), dtype=np.int32)
+        act = np.zeros(max(1, n), dtype=np.uint8)
+        cnt, imm, pend = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        N.check(self._lib.kvf_victim_select(self.h, C.byref(tv), C.byref(req), idx.ctypes.data, act.ctypes.data,
+                                            C.byref(cnt), C.byref(imm), C.byref(pend)))
+        k = cnt.value
+        return idx[:k].copy(), act[:k].copy(), imm.value, pend.value
+
+
+def depth_from_parent(parent):
+    parent = np.asarray(parent)
+    d = np.zeros(len(parent), dtype=np.uint16)
+    for i in range(1, len(parent)):
+        d[i] = d[parent[i]] + 1
+    return d

@@ -1,0 +1,197 @@
+"""Parity of the CUDA engine (libkvflow.so, via its C-ABI) against the CPU oracle.
+
+Bytes: bit-exact against the oracle's payload restatement and memcpy restatement over
+the same slot-run tables (K1 H2D gather, K2 D2H scatter, K3 HBM gather/scatter), in all
+copy back-ends.  Decisions: K4/K5 equal to the golden vectors of the UNMODIFIED reference.
+"""
+import numpy as np
+import pytest
+
+from oracle_ffi import Geom, lib as olib, load_jsonl, runs_array as oruns, TreeArrays
+
+pytestmark = pytest.mark.gpu
+
+N = pytest.importorskip("paper_2507_07400_b200._native")
+from paper_2507_07400_b200.engine import Engine, depth_from_parent  # noqa: E402
+
+MODES = [N.KVF_COPY_SM_VEC, N.KVF_COPY_SM_BULK, N.KVF_COPY_CE]
+
+
+def oracle_geom(e):
+    g = e.geom
+    return Geom(g.layers, g.kv_heads_local, g.head_dim, g.head_offset)
+
+
+def expected_bytes(e, cids):
+    """Logical [plane][token][bytes] image of a node whose tokens have content ids cids."""
+    L = olib()
+    n = len(cids)
+    buf = np.zeros(n * e.token_bytes, dtype=np.uint8)
+    L.kvfo_fill(oracle_geom(e), buf.ctypes.data, n, oruns([(0, n)]), 1,
+                np.ascontiguousarray(cids, dtype=np.uint64).ctypes.data)
+    return buf
+
+
+def rand_cids(rng, n):
+    return rng.integers(0, 2**63, size=n, dtype=np.uint64)
+
+
+def fragment(e, tier, ntok, rng, pieces=5):
+    """Allocate ntok slots as several runs by allocating/freeing a checkerboard first."""
+    blockers = []
+    runs = []
+    left = ntok
+    while left > 0:
+        take = min(left, int(rng.integers(1, max(2, ntok // pieces + 2))))
+        runs += e.alloc(tier, take)
+        blockers += e.alloc(tier, int(rng.integers(1, 4)))
+        left -= take
+    e.free(tier, blockers)
+    return runs
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = Engine(layers=4, kv_heads_total=8, head_dim=128, gpu_slots=8192, host_slots=16384)
+    yield e
+    e.close()
+
+
+def test_fill_matches_oracle_payload(eng):
+    rng = np.random.default_rng(1)
+    cids = rand_cids(rng, 777)
+    for tier in (N.KVF_TIER_DEVICE, N.KVF_TIER_HOST):
+        runs = fragment(eng, tier, len(cids), rng)
+        assert len(runs) > 1
+        eng.fill(tier, runs, cids)
+        got = eng.read(tier, runs)
+        assert np.array_equal(got, expected_bytes(eng, cids))
+        L = olib()
+        want = L.kvfo_checksum_expected(oracle_geom(eng), cids.ctypes.data, len(cids))
+        assert eng.checksum(tier, runs) == want
+        eng.free(tier, runs)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_h2d_d2h_roundtrip_bit_exact(eng, mode):
+    """K2 then K1 through fragmented runs on both tiers: bytes equal the oracle's memcpy."""
+    rng = np.random.default_rng(2 + mode)
+    eng.set_copy_mode(mode)
+    L = olib()
+    for ntok in (1, 7, 300, 2048):
+        cids = rand_cids(rng, ntok)
+        d0 = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng)
+        eng.fill(N.KVF_TIER_DEVICE, d0, cids)
+        h = fragment(eng, N.KVF_TIER_HOST, ntok, rng)
+        j = eng.d2h(d0, h)
+        eng.wait(j)
+        eng.release(j)
+        # host pool bytes == oracle memcpy of the device image into the same host runs
+        host = eng.host_pool_array()
+        want_host = np.zeros_like(host)
+        img = expected_bytes(eng, cids)
+        L.kvfo_copy_runs(oracle_geom(eng), img.ctypes.data, ntok, oruns([(0, ntok)]), 1, want_host.ctypes.data,
+                         eng.host_slots, oruns(h), len(h), 1)
+        for s, l in h:  # compare only the node's bytes, plane by plane
+            for p in range(eng.geom.layers * 2):
+                a = (p * eng.host_slots + s) * eng.tpb
+                b = a + l * eng.tpb
+                assert np.array_equal(host[a:b], want_host[a:b])
+        d1 = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng)
+        j = eng.h2d(h, d1)
+        eng.wait(j)
+        assert eng.elapsed_ms(j) > 0
+        eng.release(j)
+        assert np.array_equal(eng.read(N.KVF_TIER_DEVICE, d1), img)
+        for t, r in ((N.KVF_TIER_DEVICE, d0), (N.KVF_TIER_HOST, h), (N.KVF_TIER_DEVICE, d1)):
+            eng.free(t, r)
+    eng.set_copy_mode(N.KVF_COPY_SM_VEC)
+
+
+def test_many_pieces_split_launches(eng):
+    """> 48 pieces per job: the engine splits launches; bytes still exact."""
+    rng = np.random.default_rng(5)
+    ntok = 400
+    cids = rand_cids(rng, ntok)
+    h = fragment(eng, N.KVF_TIER_HOST, ntok, rng, pieces=150)
+    assert len(h) > 48
+    eng.fill(N.KVF_TIER_HOST, h, cids)
+    d = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng, pieces=90)
+    for mode in MODES:
+        eng.set_copy_mode(mode)
+        j = eng.h2d(h, d)
+        eng.wait(j)
+        eng.release(j)
+        assert np.array_equal(eng.read(N.KVF_TIER_DEVICE, d), expected_bytes(eng, cids))
+    eng.set_copy_mode(N.KVF_COPY_SM_VEC)
+    eng.free(N.KVF_TIER_HOST, h)
+    eng.free(N.KVF_TIER_DEVICE, d)
+
+
+def test_dev_gather_scatter_k3(eng):
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(6)
+    ntok = 1500
+    cids = rand_cids(rng, ntok)
+    d = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng)
+    eng.fill(N.KVF_TIER_DEVICE, d, cids)
+    stage = torch.zeros(ntok * eng.token_bytes, dtype=torch.uint8, device="cuda")
+    j = eng.dev_gather(d, stage.data_ptr())
+    eng.wait(j)
+    eng.release(j)
+    torch.cuda.synchronize()
+    assert np.array_equal(stage.cpu().numpy(), expected_bytes(eng, cids))
+    d2 = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng)
+    j = eng.dev_scatter(stage.data_ptr(), d2)
+    eng.wait(j)
+    eng.release(j)
+    assert np.array_equal(eng.read(N.KVF_TIER_DEVICE, d2), expected_bytes(eng, cids))
+    eng.free(N.KVF_TIER_DEVICE, d)
+    eng.free(N.KVF_TIER_DEVICE, d2)
+
+
+def test_empty_and_invalid_jobs(eng):
+    j = eng.h2d([], [])
+    eng.wait(j)
+    eng.release(j)
+    with pytest.raises(N.KvfError):
+        eng.h2d([(0, 4)], [(0, 5)])  # token counts differ
+    with pytest.raises(N.KvfError):
+        eng.h2d([(eng.host_slots, 1)], [(0, 1)])  # out of range
+    with pytest.raises(N.KvfError):
+        eng.wait(999999)
+
+
+def test_full_pool_allocation(eng):
+    free, _ = eng.free_count(N.KVF_TIER_DEVICE)
+    runs = eng.alloc(N.KVF_TIER_DEVICE, free)
+    with pytest.raises(N.KvfError) as ex:
+        eng.alloc(N.KVF_TIER_DEVICE, 1)
+    assert ex.value.code == 10  # OutOfGpuMemory + 1
+    eng.free(N.KVF_TIER_DEVICE, runs)
+    assert eng.free_count(N.KVF_TIER_DEVICE) == (free, 1)
+
+
+def test_k4_priority_matches_reference(eng):
+    for c in load_jsonl("prio.jsonl"):
+        b = c["boundaries"]
+        got = eng.priority(c["parent"], [x[0] for x in b], [int(x[1]) for x in b])
+        want = np.asarray([int(x) for x in c["rank"]], dtype=np.int64)
+        assert np.array_equal(got[1:], want[1:]), c["case"]
+
+
+@pytest.mark.parametrize("fixture", ["evict_small.jsonl", "evict_medium.jsonl", "evict_bounded.jsonl"])
+def test_k5_victims_match_reference(eng, fixture):
+    for c in load_jsonl(fixture):
+        if "error" in c:
+            continue
+        ta = TreeArrays(c)
+        tree = {k: getattr(ta, k) for k in ("parent", "status", "lock", "rank", "time", "seq", "id", "tokens",
+                                            "backed")}
+        tree["depth"] = depth_from_parent(ta.parent)
+        tree["bpt"] = ta.bpt
+        idx, act, imm, pend = eng.victims(tree, c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"],
+                                          c["cpu_used"], c["cpu_cap"])
+        got = [(int(ta.id[v]), int(ta.tokens[v]) * ta.bpt, 0 if a == 0 else 1) for v, a in zip(idx, act)]
+        assert got == [tuple(v) for v in c["victims"]], (fixture, c["case"])
+        assert (imm, pend) == (c["immediate"], c["pending"])
