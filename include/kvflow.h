@@ -183,6 +183,9 @@ int kvf_fill_payload(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t 
                      uint64_t ntok);
 /* Order-independent checksum of a node's bytes in logical (plane, token, byte) order.  Sync. */
 int kvf_checksum(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs, uint64_t* out);
+/* The checksum a node with content ids cids[0..ntok) must have (no buffer; computed on the
+ * GPU from the payload definition).  Sync. */
+int kvf_payload_checksum(kvf_engine* e, const uint64_t* cids, uint64_t ntok, uint64_t* out);
 /* Copies a node's bytes in logical order into a host buffer of ntok*token_bytes bytes.  Sync. */
 int kvf_read_runs(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n_runs, void* dst, uint64_t dst_bytes);
 

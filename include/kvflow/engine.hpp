@@ -59,6 +59,7 @@ public:
 
     void fill(int tier, const RunList& runs, const std::vector<uint64_t>& cids);
     uint64_t checksum(int tier, const RunList& runs);
+    uint64_t payload_checksum(const std::vector<uint64_t>& cids);
 
     std::vector<int64_t> priorities(const std::vector<int32_t>& parent, const std::vector<int32_t>& bidx,
                                     const std::vector<int64_t>& cand);

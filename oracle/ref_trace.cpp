@@ -137,10 +137,12 @@ int run_sim(const std::map<std::string, std::string>& kv) {
 
     Simulator sim(cost, sc, w, gpu_cap, cpu_cap, seed);
     uint64_t ev = 0;
+    std::string args;
+    for (const auto& [k, v] : kv) args += (args.empty() ? "" : ",") + jstr(k) + ":" + jstr(v);
     std::printf("{\"t\":\"cfg\",\"workload\":%s,\"policy\":%s,\"bpt\":%" PRIu64 ",\"gpu_cap\":%" PRIu64
-                ",\"cpu_cap\":%" PRIu64 ",\"seed\":%" PRIu64 ",\"profile\":%s}\n",
+                ",\"cpu_cap\":%" PRIu64 ",\"seed\":%" PRIu64 ",\"profile\":%s,\"args\":{%s}}\n",
                 jstr(w.label()).c_str(), jstr(policy_name(sc.policy)).c_str(), cost.bytes_per_token, gpu_cap, cpu_cap,
-                seed, jstr(prof).c_str());
+                seed, jstr(prof).c_str(), args.c_str());
     auto prev = sim.tier().transition_observer;
     sim.tier().transition_observer = [&](const CacheNode& n, NodeStatus from, NodeStatus to) {
         std::printf("{\"t\":\"tr\",\"ev\":%" PRIu64 ",\"node\":%" PRIu64 ",\"from\":%d,\"to\":%d,\"tokens\":%zu}\n", ev,

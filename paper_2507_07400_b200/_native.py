@@ -92,6 +92,7 @@ _ENGINE_SIGS = {
                                     C.POINTER(C.c_uint64)]),
     "kvf_fill_payload": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_checksum": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.POINTER(C.c_uint64)]),
+    "kvf_payload_checksum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "kvf_read_runs": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_get_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
 }

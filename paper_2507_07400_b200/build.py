@@ -57,7 +57,7 @@ def build_host(force=False):
     if force or _stale(out, deps):
         _run(["g++", "-std=c++20", "-O2", "-g", "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter",
               f"-I{INC}", *srcs, "-o", out, f"-L{PKG}", "-lkvflow", "-Wl,-rpath,$ORIGIN",
-              "-L/usr/local/cuda/lib64", "-lcudart"])
+              ])
     return out
 
 

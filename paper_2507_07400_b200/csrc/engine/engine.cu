@@ -406,6 +406,29 @@ __global__ void kvf_checksum_kernel(const char* pool, uint64_t plane_stride, uin
     if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(acc));
 }
 
+__global__ void kvf_payload_checksum_kernel(uint32_t tpb, uint32_t planes, uint32_t wph, uint32_t head_offset,
+                                            const uint64_t* __restrict__ cids, uint64_t ntok,
+                                            unsigned long long* out) {
+    const uint32_t wpt = tpb / 8;
+    const uint64_t total = static_cast<uint64_t>(planes) * ntok * wpt;
+    uint64_t acc = 0;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t per_plane = ntok * wpt;
+        const uint32_t plane = static_cast<uint32_t>(w / per_plane);
+        const uint64_t r = w - plane * per_plane;
+        const uint64_t k = r / wpt;
+        const uint32_t j = static_cast<uint32_t>(r - k * wpt);
+        const uint32_t h = j / wph, wi = j - h * wph;
+        const uint64_t base =
+            mix64(cids[k] ^ (static_cast<uint64_t>(plane) * 0x100000001b3ULL) ^ (static_cast<uint64_t>(head_offset + h) << 48));
+        const uint64_t word = mix64(base + wi) & 0xBFFFBFFFBFFFBFFFULL;
+        acc += mix64(word ^ (w * 0x9e3779b97f4a7c15ULL));
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, static_cast<unsigned long long>(acc));
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -523,7 +546,9 @@ int transfer(kvf_engine* e, uint64_t job_id, int src_tier, const kvf_run* src_ru
     Job j;
     int rc = begin_job(e, job_id, st, j);
     if (rc) return rc;
-    if (d2h && e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(st, e->dev_write_done, 0));
+    // Order against the compute stream's last payload write (fill / K3 scatter): a D2H may
+    // read those slots, an H2D may land in slots a just-discarded node's fill still targets.
+    if ((d2h || h2d) && e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(st, e->dev_write_done, 0));
     const uint64_t stride_s = tier_slots(e, src_tier) * e->tpb, stride_d = tier_slots(e, dst_tier) * e->tpb;
     Endpoint src{tier_base(e, src_tier), stride_s, src_tier == KVF_TIER_HOST};
     Endpoint dst{tier_base(e, dst_tier), stride_d, dst_tier == KVF_TIER_HOST};
@@ -881,6 +906,28 @@ int kvf_checksum(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t n, u
     kvf_checksum_kernel<<<grid_for(e, words, 256), 256, 0, e->s_dev>>>(
         tier_base(e, tier), tier_slots(e, tier) * e->tpb, static_cast<uint32_t>(e->tpb), e->planes, d_slots, ntok,
         reinterpret_cast<unsigned long long*>(e->d_checksum));
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    KVF_CUDA(cudaMemcpyAsync(out, e->d_checksum, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s_dev));
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    return KVF_OK;
+}
+
+int kvf_payload_checksum(kvf_engine* e, const uint64_t* cids, uint64_t ntok, uint64_t* out) {
+    KVF_GUARD(e);
+    if (!out || (ntok && !cids)) return set_error(KVF_E_INVALID_ARG, "bad argument");
+    *out = 0;
+    if (ntok == 0) return KVF_OK;
+    KVF_CUDA(cudaStreamSynchronize(e->s_dev));
+    int rc = e->ws_dev.ensure(ntok * 8 + 64, ntok * 8 + 64);
+    if (rc) return rc;
+    std::memcpy(e->ws_dev.host, cids, ntok * 8);
+    KVF_CUDA(cudaMemcpyAsync(e->ws_dev.dev, e->ws_dev.host, ntok * 8, cudaMemcpyHostToDevice, e->s_dev));
+    KVF_CUDA(cudaMemsetAsync(e->d_checksum, 0, sizeof(uint64_t), e->s_dev));
+    const uint64_t words = static_cast<uint64_t>(e->planes) * ntok * (e->tpb / 8);
+    kvf_payload_checksum_kernel<<<grid_for(e, words, 256), 256, 0, e->s_dev>>>(
+        static_cast<uint32_t>(e->tpb), e->planes, e->geom.head_dim / 4, e->geom.head_offset,
+        static_cast<const uint64_t*>(e->ws_dev.dev), ntok, reinterpret_cast<unsigned long long*>(e->d_checksum));
     KVF_CUDA(cudaGetLastError());
     e->stats.kernel_launches++;
     KVF_CUDA(cudaMemcpyAsync(out, e->d_checksum, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->s_dev));
