@@ -143,6 +143,12 @@ class Engine:
         N.check(self._lib.kvf_checksum(self.h, tier, N.runs_array(runs), len(runs), C.byref(out)))
         return out.value
 
+    def payload_checksum(self, cids):
+        cids = np.ascontiguousarray(cids, dtype=np.uint64)
+        out = C.c_uint64()
+        N.check(self._lib.kvf_payload_checksum(self.h, cids.ctypes.data, len(cids), C.byref(out)))
+        return out.value
+
     def read(self, tier, runs):
         ntok = sum(l for _, l in runs)
         buf = np.zeros(ntok * self.token_bytes, dtype=np.uint8)
