@@ -194,6 +194,8 @@ typedef struct {
     uint64_t kernel_launches; /* every kernel this engine launched */
     uint64_t h2d_bytes, d2h_bytes, dev_bytes;
     uint64_t h2d_jobs, d2h_jobs, dev_jobs, decisions;
+    double decision_kernel_ms; /* K4+K5 kernel time, CUDA events on the decision stream */
+    double decision_call_us;   /* K4+K5 host round trip (pack, H2D, kernel, D2H, sync)  */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

@@ -59,7 +59,8 @@ class EvictRequest(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("dev_bytes", C.c_uint64), ("h2d_jobs", C.c_uint64), ("d2h_jobs", C.c_uint64),
-                ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64)]
+                ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
+                ("decision_call_us", C.c_double)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature

@@ -13,12 +13,14 @@
 //        eff(n)      = max(ord(n), eff(device children))   ord = position in `before` order
 //        victims     = R sorted by (eff asc, depth desc), cut at the first prefix whose
 //                      byte sum reaches `needed`.
-//     One CTA: bitonic sort of the candidates by the 4-word key, a bottom-up level sweep
-//     (shared-memory atomics) for R/eff, a bitonic sort of 64-bit (eff, depth, idx) keys,
-//     and a block scan for the byte cut.
+//     One CTA, everything in shared memory: a bitonic sort of the candidates by the
+//     4-word key, R and eff by parallel root walks (shared-memory atomics with early
+//     exit, no per-level barriers), a bitonic sort of 64-bit (eff, depth, idx) keys, and
+//     a block scan for the byte cut.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "engine_internal.hpp"
@@ -72,39 +74,6 @@ struct OutDev {
     unsigned long long* header;  // [count, immediate, pending]
 };
 
-// Strict total order of radix_cache.cpp:316-321 (`before`); 0xFFFF pads sort last.
-__device__ __forceinline__ bool before(const TreeDev& t, bool wa, uint32_t a, uint32_t b) {
-    if (b == 0xFFFFu) return a != 0xFFFFu;
-    if (a == 0xFFFFu) return false;
-    if (wa) {
-        const int64_t ra = __ldg(t.rank + a), rb = __ldg(t.rank + b);
-        if (ra != rb) return ra > rb;
-    }
-    const double ta = __ldg(t.time + a), tb = __ldg(t.time + b);
-    if (ta != tb) return ta < tb;
-    const uint64_t sa = __ldg(t.seq + a), sb = __ldg(t.seq + b);
-    if (sa != sb) return sa < sb;
-    return __ldg(t.id + a) < __ldg(t.id + b);
-}
-
-__device__ __forceinline__ void bitonic_idx(uint16_t* a, uint32_t P, const TreeDev& t, bool wa) {
-    for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                const uint32_t l = i ^ j;
-                if (l > i) {
-                    const bool up = (i & k) == 0;
-                    const uint16_t x = a[i], y = a[l];
-                    if (before(t, wa, y, x) == up) {
-                        a[i] = y;
-                        a[l] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-}
-
 __device__ __forceinline__ void bitonic_u64(uint64_t* a, uint32_t P) {
     for (uint32_t k = 2; k <= P; k <<= 1)
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -129,91 +98,135 @@ __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
     return p;
 }
 
-// dynamic smem layout for n <= 4096 (P = 4096):
-//   keys u64[P] | pref u64[P] | ord i32[n] | cmax i32[n] | sel u16[P] | flags u8[n]
+// Shared-memory layout for n <= 4096 nodes (PN = pow2 >= n):
+//   region A (32*PN B): phase-1 sort keys time|seq|id|rank per node, later reused for the
+//                       final 64-bit victim keys and the byte prefix
+//   region B:           parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | sel u16[PN]
+//                       | status u8[n] | flags u8[n]
+// flags: bit0 selfok, bit1 releases, bit2 R
 __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, const ReqDev q, OutDev o) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t n = t.n;
     const uint32_t PN = pow2_ceil(n > 1 ? n : 2);
-    uint64_t* keys = reinterpret_cast<uint64_t*>(sm);
+    double* k_time = reinterpret_cast<double*>(sm);
+    uint64_t* k_seq = reinterpret_cast<uint64_t*>(k_time + PN);
+    uint64_t* k_id = k_seq + PN;
+    int64_t* k_rank = reinterpret_cast<int64_t*>(k_id + PN);
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm);  // phase 3 reuse of region A
     uint64_t* pref = keys + PN;
-    int32_t* ord = reinterpret_cast<int32_t*>(pref + PN);
-    int32_t* cmax = ord + n;
-    uint16_t* sel = reinterpret_cast<uint16_t*>(cmax + n);
-    uint8_t* flags = reinterpret_cast<uint8_t*>(sel + PN);  // bit0 selfok, bit2 R (owner-written only)
-    __shared__ uint32_t s_cnt, s_rcnt, s_maxd;
+    int32_t* parent = reinterpret_cast<int32_t*>(k_rank + PN);
+    int32_t* ord = parent + n;
+    int32_t* eff = ord + n;
+    uint32_t* blocked = reinterpret_cast<uint32_t*>(eff + n);
+    uint16_t* sel = reinterpret_cast<uint16_t*>(blocked + n);
+    uint8_t* st = reinterpret_cast<uint8_t*>(sel + PN);
+    uint8_t* flags = st + n;
+    __shared__ uint32_t s_cnt, s_rcnt;
     __shared__ unsigned long long s_imm, s_pend, s_warp[kThreads / 32];
     if (threadIdx.x == 0) {
         s_cnt = 0;
         s_rcnt = 0;
-        s_maxd = 0;
         s_imm = 0;
         s_pend = 0;
     }
     __syncthreads();
-    // 1. self-eligibility (radix_cache.cpp:305-312 minus the device-child test) + compaction
+    const bool wa = q.wa != 0;
+    // 1. stage the snapshot; self-eligibility (radix_cache.cpp:305-312 minus the device-child
+    //    test) and whether evicting the node frees its parent (Discard / backed / CPU full)
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        uint8_t f = 0;
-        if (i > 0 && t.lock[i] == 0 && t.status[i] == 0 && (!q.has_floor || t.rank[i] > q.floor)) f = 1;
-        flags[i] = f;
-        cmax[i] = -1;
+        const uint8_t s = t.status[i];
+        const uint64_t bytes = t.tokens[i] * t.bpt;
+        const bool cpu_room = q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap;
+        const bool selfok = i > 0 && t.lock[i] == 0 && s == 0 && (!q.has_floor || t.rank[i] > q.floor);
+        const bool releases = !q.offload || t.backed[i] || !cpu_room;
+        parent[i] = t.parent[i];
+        st[i] = s;
+        flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
+        blocked[i] = 0;
         ord[i] = -1;
-        if (f) sel[atomicAdd(&s_cnt, 1u)] = static_cast<uint16_t>(i);
-        if (i > 0) atomicMax(&s_maxd, static_cast<uint32_t>(t.depth[i]));
+        k_time[i] = t.time[i];
+        k_seq[i] = t.seq[i];
+        k_id[i] = t.id[i];
+        k_rank[i] = t.rank[i];
+        if (selfok) sel[atomicAdd(&s_cnt, 1u)] = static_cast<uint16_t>(i);
     }
     __syncthreads();
     const uint32_t c = s_cnt;
     const uint32_t P = pow2_ceil(c > 1 ? c : 2);
     for (uint32_t i = c + threadIdx.x; i < P; i += blockDim.x) sel[i] = 0xFFFFu;
     __syncthreads();
-    // 2. candidates in `before` order -> ord
-    bitonic_idx(sel, P, t, q.wa != 0);
+    // 2. candidates in `before` order (radix_cache.cpp:316-321) -> ord
+    for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l <= i) continue;
+                const uint32_t x = sel[i], y = sel[l];
+                bool y_first;
+                if (x == 0xFFFFu) y_first = y != 0xFFFFu;
+                else if (y == 0xFFFFu) y_first = false;
+                else if (wa && k_rank[x] != k_rank[y]) y_first = k_rank[y] > k_rank[x];
+                else if (k_time[x] != k_time[y]) y_first = k_time[y] < k_time[x];
+                else if (k_seq[x] != k_seq[y]) y_first = k_seq[y] < k_seq[x];
+                else y_first = k_id[y] < k_id[x];
+                if (y_first == ((i & k) == 0)) {
+                    sel[i] = static_cast<uint16_t>(y);
+                    sel[l] = static_cast<uint16_t>(x);
+                }
+            }
+            __syncthreads();
+        }
     for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) ord[sel[k]] = static_cast<int32_t>(k);
+    // 3. blocked(n): some node of n's device subtree (below n) is not self-eligible or would
+    //    not release it (has_device_child, radix_cache.cpp:40-45).  Every such node walks up
+    //    through device-child links; a walker stops where another already passed.
+    for (uint32_t m = threadIdx.x + 1; m < n; m += blockDim.x) {
+        const uint8_t f = flags[m];
+        if (st[m] == 1 || ((f & 1) && (f & 2))) continue;  // BACKUP children never block
+        for (int32_t cur = static_cast<int32_t>(m);;) {
+            const int32_t p = parent[cur];
+            if (p <= 0) break;
+            if (atomicOr(&blocked[p], 1u)) break;
+            if (st[p] == 1) break;
+            cur = p;
+        }
+    }
     __syncthreads();
-    // 3. bottom-up level sweep: R(n) and eff(n); a blocked or non-releasing device child
-    //    pins its parent (has_device_child, radix_cache.cpp:40-45) by raising the parent's
-    //    child-max to kBlocked.
-    for (int d = static_cast<int>(s_maxd); d >= 1; --d) {
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            if (t.depth[i] != d) continue;
-            const uint8_t f = flags[i];
-            const bool r = (f & 1) && cmax[i] != kBlocked;
-            const int32_t e = r ? max(ord[i], cmax[i]) : -1;
-            if (r) {
-                flags[i] = f | 4;
-                cmax[i] = e;  // cmax now holds eff(i)
-            }
-            if (t.status[i] != 1) {
-                const uint64_t bytes = t.tokens[i] * t.bpt;
-                const bool cpu_room = q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap;
-                const bool releases = !q.offload || t.backed[i] || !cpu_room;
-                const int32_t p = t.parent[i];
-                atomicMax(&cmax[p], (r && releases) ? e : kBlocked);
-            }
-        }
-        __syncthreads();
-    }
-    // 4. R nodes keyed by (eff asc, depth desc, idx) -- unique per node
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        if (flags[i] & 4) {
-            const uint64_t key = (static_cast<uint64_t>(cmax[i]) << 32) |
-                                 (static_cast<uint64_t>(0xFFFFu - t.depth[i]) << 16) | i;
-            keys[atomicAdd(&s_rcnt, 1u)] = key;
+        const bool r = (flags[i] & 1) && !blocked[i];
+        if (r) flags[i] |= 4;
+        eff[i] = r ? ord[i] : -1;
+    }
+    __syncthreads();
+    // 4. eff(n) = max ord over n's device subtree (all of it is in R when n is): R nodes push
+    //    their ord up while the ancestor is in R; stop when an ancestor already holds more.
+    for (uint32_t m = threadIdx.x + 1; m < n; m += blockDim.x) {
+        if (!(flags[m] & 4)) continue;
+        const int32_t v = ord[m];
+        for (int32_t cur = static_cast<int32_t>(m);;) {
+            const int32_t p = parent[cur];
+            if (p <= 0 || !(flags[p] & 4)) break;
+            if (atomicMax(&eff[p], v) >= v) break;
+            cur = p;
         }
     }
+    __syncthreads();
+    // 5. victims = R sorted by (eff asc, depth desc); keys are unique per node
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (flags[i] & 4)
+            keys[atomicAdd(&s_rcnt, 1u)] = (static_cast<uint64_t>(eff[i]) << 32) |
+                                            (static_cast<uint64_t>(0xFFFFu - t.depth[i]) << 16) | i;
     __syncthreads();
     const uint32_t r = s_rcnt;
     const uint32_t PR = pow2_ceil(r > 1 ? r : 2);
     for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
     __syncthreads();
     bitonic_u64(keys, PR);
-    // 5. exclusive byte prefix in victim order (block scan, 4 items/thread max)
+    // 6. exclusive byte prefix in victim order (block scan, <= 4 items per thread)
     const uint32_t per = (r + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo_k = threadIdx.x * per, hi_k = min(r, (threadIdx.x + 1) * per);
     uint64_t local = 0;
-    for (uint32_t k = threadIdx.x * per; k < min(r, (threadIdx.x + 1) * per); ++k) {
-        const uint32_t v = static_cast<uint32_t>(keys[k] & 0xFFFFu);
-        local += t.tokens[v] * t.bpt;
-    }
+    for (uint32_t k = lo_k; k < hi_k; ++k) local += t.tokens[keys[k] & 0xFFFFu] * t.bpt;
     uint64_t inc = local;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int off = 1; off < 32; off <<= 1) {
@@ -232,9 +245,8 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     }
     __syncthreads();
     uint64_t run = inc - local + (warp ? s_warp[warp - 1] : 0);
-    // 6. cut: victim k is popped iff the bytes freed before it are < needed
-    //    (the loop condition of radix_cache.cpp:335)
-    for (uint32_t k = threadIdx.x * per; k < min(r, (threadIdx.x + 1) * per); ++k) {
+    // 7. victim k is popped iff the bytes freed before it are still < needed (radix_cache.cpp:335)
+    for (uint32_t k = lo_k; k < hi_k; ++k) {
         const uint32_t v = static_cast<uint32_t>(keys[k] & 0xFFFFu);
         const uint64_t bytes = t.tokens[v] * t.bpt;
         if (run < q.needed) {
@@ -255,23 +267,29 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t cnt = 0;
-        // taken victims form a prefix; count them
-        uint32_t lo = 0, hi = r;
+        uint32_t lo = 0, hi = r;  // taken victims form a prefix
         while (lo < hi) {
             const uint32_t mid = (lo + hi) / 2;
             if (pref[mid]) lo = mid + 1; else hi = mid;
         }
-        cnt = lo;
-        o.header[0] = cnt;
+        o.header[0] = lo;
         o.header[1] = s_imm;
         o.header[2] = s_pend;
     }
 }
 
 size_t victim_smem(uint32_t n) {
-    const uint32_t PN = pow2_ceil(n > 1 ? n : 2);
-    return PN * 8 * 2 + static_cast<size_t>(n) * 4 * 2 + PN * 2 + ((n + 3) & ~3u) + 16;
+    const size_t PN = pow2_ceil(n > 1 ? n : 2);
+    return PN * 32 + static_cast<size_t>(n) * 16 + PN * 2 + 2 * ((n + 15) & ~15u) + 64;
+}
+
+int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
+    float ms = 0;
+    KVF_CUDA(cudaEventElapsedTime(&ms, e->dec_start, e->dec_stop));
+    e->stats.decision_kernel_ms += ms;
+    e->stats.decision_call_us +=
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    return KVF_OK;
 }
 
 template <typename T>
@@ -291,11 +309,12 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     std::lock_guard<std::mutex> lk(e->mu);
     if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
     if (n == 0) return KVF_OK;
+    const auto t0 = std::chrono::steady_clock::now();
     for (uint32_t b = 0; b < m; ++b)
         if (bidx[b] < 0 || static_cast<uint32_t>(bidx[b]) >= n) return set_error(KVF_E_UNKNOWN_BOUNDARY_NODE, "boundary index out of range");
     const size_t in_bytes = ((n * 4 + 15) & ~15ull) + ((m * 4 + 15) & ~15ull) + m * 8 + 16;
     const size_t out_bytes = n * 8;
-    int rc = e->ws_dec.ensure(in_bytes + out_bytes + 1024, in_bytes + 1024);
+    int rc = e->ws_dec.ensure(in_bytes + out_bytes + 1024, in_bytes + out_bytes + 1024);
     if (rc) return rc;
     char* h = static_cast<char*>(e->ws_dec.host);
     char* hp = h;
@@ -310,13 +329,17 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     int64_t* d_cand = carve<int64_t>(dp, m);
     long long* d_out = reinterpret_cast<long long*>(d + ((used + 255) & ~size_t(255)));
     KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
+    KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     kvf_priority_kernel<<<1, kThreads, 0, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out);
     KVF_CUDA(cudaGetLastError());
+    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;
-    KVF_CUDA(cudaMemcpyAsync(out_rank, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
+    // results land in pinned staging (a pageable destination would force a staged copy)
+    KVF_CUDA(cudaMemcpyAsync(h, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
-    return KVF_OK;
+    std::memcpy(out_rank, h, n * 8);
+    return finish_decision(e, t0);
 }
 
 int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
@@ -331,6 +354,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     if (n <= 1 || q->needed == 0) return KVF_OK;
     if (n > kMaxNodesSingleCta)
         return set_error(KVF_E_TOO_LARGE, "victim selection above 4096 nodes needs the multi-CTA path");
+    const auto t0 = std::chrono::steady_clock::now();
     // pack the SoA snapshot into one pinned buffer -> one H2D copy
     const size_t in_bytes = 5 * ((n * 8 + 15) & ~15ull) + 2 * ((n * 4 + 15) & ~15ull) + ((n * 2 + 15) & ~15ull) +
                             2 * ((n + 15) & ~15ull);
@@ -379,8 +403,10 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
                                       static_cast<int>(victim_smem(kMaxNodesSingleCta))));
         attr = victim_smem(kMaxNodesSingleCta);
     }
+    KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     kvf_victim_kernel<<<1, kThreads, smem, e->s_dec>>>(td, rq, od);
     KVF_CUDA(cudaGetLastError());
+    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;
     char* hout = h + ((used + 255) & ~size_t(255));
@@ -393,7 +419,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     *out_count = cnt;
     *out_imm = hdr[1];
     *out_pend = hdr[2];
-    return KVF_OK;
+    return finish_decision(e, t0);
 }
 
 }  // extern "C"

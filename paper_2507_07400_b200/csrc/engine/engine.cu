@@ -479,8 +479,12 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         p.planes = e->planes;
         p.npieces = np;
         const bool vec16 = (tpb % 16) == 0;
-        uint32_t threads = 512, unroll = 8;
-        p.tile_bytes = threads * unroll * (vec16 ? 16 : 8);  // 64 KiB (16-B vectors)
+        // PCIe jobs keep ~the link's bandwidth-delay product in flight (8 CTAs x 256 thr x 4 x
+        // 16 B = 128 KiB): full H2D rate, and 7x lower queueing for concurrent small H2D
+        // traffic such as decision inputs (profiles/r01_probe_inflight.txt).  HBM jobs go wide.
+        const bool pcie = src.host || dst.host;
+        const uint32_t threads = pcie ? 256 : 512, unroll = pcie ? 4 : 8;
+        p.tile_bytes = threads * unroll * (vec16 ? 16 : 8);
         uint64_t tiles = 0;
         for (uint32_t i = 0; i < np; ++i) {
             const Piece& pc = pieces[first + i];
@@ -504,7 +508,8 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
             }
             kvf_copy_bulk_kernel<kBulkStages, kBulkChunk><<<grid, 32, smem, stream>>>(p);
         } else if (vec16) {
-            kvf_copy_vec_kernel<uint4, 8><<<grid, threads, 0, stream>>>(p);
+            if (pcie) kvf_copy_vec_kernel<uint4, 4><<<grid, threads, 0, stream>>>(p);
+            else kvf_copy_vec_kernel<uint4, 8><<<grid, threads, 0, stream>>>(p);
         } else {
             kvf_copy_vec_kernel<uint2, 8><<<grid, threads, 0, stream>>>(p);
         }
@@ -664,7 +669,7 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
     if (cudaSetDevice(e->device) != cudaSuccess) return fail(set_error(KVF_E_CUDA, "cudaSetDevice"));
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, e->device) == cudaSuccess) e->sm_count = prop.multiProcessorCount;
-    if (e->cfg.pcie_ctas == 0) e->cfg.pcie_ctas = 32;
+    if (e->cfg.pcie_ctas == 0) e->cfg.pcie_ctas = 8;
     if (e->cfg.hbm_ctas == 0) e->cfg.hbm_ctas = static_cast<uint32_t>(e->sm_count) * 4;
     cudaError_t err;
     e->dev_slots = cfg->gpu_slots;
@@ -706,7 +711,8 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
         (err = cudaStreamCreateWithFlags(&e->s_dev, cudaStreamNonBlocking)) != cudaSuccess ||
         (err = cudaStreamCreateWithPriority(&e->s_dec, cudaStreamNonBlocking, hi)) != cudaSuccess)
         return fail(cuda_error(err, "cudaStreamCreate"));
-    if ((err = cudaEventCreateWithFlags(&e->dev_write_done, cudaEventDisableTiming)) != cudaSuccess)
+    if ((err = cudaEventCreateWithFlags(&e->dev_write_done, cudaEventDisableTiming)) != cudaSuccess ||
+        (err = cudaEventCreate(&e->dec_start)) != cudaSuccess || (err = cudaEventCreate(&e->dec_stop)) != cudaSuccess)
         return fail(cuda_error(err, "cudaEventCreate"));
     if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_checksum), sizeof(uint64_t))) != cudaSuccess)
         return fail(cuda_error(err, "cudaMalloc(checksum)"));
@@ -723,7 +729,8 @@ int kvf_engine_destroy(kvf_engine* e) {
         cudaEventDestroy(j.stop);
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
-    if (e->dev_write_done) cudaEventDestroy(e->dev_write_done);
+    for (cudaEvent_t ev : {e->dev_write_done, e->dec_start, e->dec_stop})
+        if (ev) cudaEventDestroy(ev);
     for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec})
         if (s) cudaStreamDestroy(s);
     e->ws_dev.release();

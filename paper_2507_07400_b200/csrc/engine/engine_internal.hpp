@@ -90,6 +90,7 @@ struct kvf_engine {
 
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_dev = nullptr, s_dec = nullptr;
     cudaEvent_t dev_write_done = nullptr;  // last fill / K3 scatter on s_dev
+    cudaEvent_t dec_start = nullptr, dec_stop = nullptr;  // decision kernel timing
     bool dev_write_pending = false;
 
     std::unordered_map<uint64_t, kvf_impl::Job> jobs;

@@ -1,0 +1,317 @@
+// GPU-backed unit tests of the C++ control plane: eviction order and actions (K5),
+// priorities (K4), and TierManager transfers that move real bytes (K1/K2).  Cases restate
+// the reference's radix-cache and tier-manager suites (proj/tests/test_radix_cache.cpp:143-349,
+// 435-452; test_tier_manager.cpp) on the kvf API with an Engine attached.
+#include <algorithm>
+#include <map>
+#include <numeric>
+#include <random>
+
+#include "kvflow/radix_cache.hpp"
+#include "kvflow/sim_engine.hpp"
+#include "kvflow/tier_manager.hpp"
+#include "tinytest.hpp"
+
+using namespace kvf;
+
+namespace {
+
+constexpr Bytes kBpt = 16;  // 1 layer x 1 head x 4 dims x bf16 x {K,V}
+
+Engine& engine() {
+    static Engine e([] {
+        EngineOptions o;
+        o.layers = 1;
+        o.kv_heads_total = 1;
+        o.kv_heads_local = 1;
+        o.head_dim = 4;
+        o.gpu_slots = 1 << 20;
+        o.host_slots = 1 << 20;
+        return o;
+    }());
+    return e;
+}
+
+CostModel flat_cost() {
+    CostModel c;
+    c.bytes_per_token = kBpt;
+    c.prefill_a = 1e-4;
+    c.prefill_b = 1e-3;
+    c.decode_base = 1e-3;
+    c.decode_per_seq = 1e-4;
+    c.h2d_bandwidth = 1e9;
+    c.d2h_bandwidth = 1e9;
+    c.pcie_efficiency = 1.0;
+    c.fixed_latency = 0;
+    return c;
+}
+
+struct Rig {
+    EventQueue ev;
+    TierManager tier;
+    RadixCache cache;
+    explicit Rig(Bytes cpu_cap = 0) : tier(1 << 20, cpu_cap, flat_cost(), ev, &engine()), cache(kBpt, &engine()) {}
+    InsertResult put(const TokenSeq& s, VirtualTime now) {
+        InsertResult ins = cache.insert(s, now);
+        tier.reserve_working(ins.new_bytes);
+        tier.convert_working(ins.new_bytes, ins.new_bytes);
+        return ins;
+    }
+    uint64_t id_of(const TokenSeq& key) const {
+        uint64_t id = 0;
+        cache.for_each_node([&](const CacheNode& n) {
+            if (n.key == key) id = n.id;
+        });
+        return id;
+    }
+    CacheNode* node(const TokenSeq& key) {
+        CacheNode* f = nullptr;
+        cache.for_each_node([&](const CacheNode& n) {
+            if (n.key == key) f = const_cast<CacheNode*>(&n);
+        });
+        return f;
+    }
+    // the node's HBM bytes equal its expected payload (GPU checksum vs GPU payload hash)
+    bool dev_ok(const CacheNode& n) {
+        return engine().checksum(KVF_TIER_DEVICE, n.dev_runs) == engine().payload_checksum(cache.node_cids(n));
+    }
+    bool host_ok(const CacheNode& n) {
+        return engine().checksum(KVF_TIER_HOST, n.host_runs) == engine().payload_checksum(cache.node_cids(n));
+    }
+};
+
+}  // namespace
+
+TEST("evict: LRU takes the least recently accessed first; discard frees the slots") {
+    Rig r;
+    const uint64_t free0 = engine().free_tokens(KVF_TIER_DEVICE);
+    r.put({1, 11, 12}, 1.0);
+    r.put({2, 21, 22}, 2.0);
+    r.put({3, 31, 32}, 3.0);
+    CHECK(engine().free_tokens(KVF_TIER_DEVICE) == free0 - 9);
+    const uint64_t a = r.id_of({1, 11, 12});
+    EvictOutcome out = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 4.0);
+    REQUIRE(out.victims.size() == 1);
+    CHECK(out.victims[0].node_id == a);
+    CHECK(out.victims[0].immediate);
+    CHECK(out.immediate_freed == 3 * kBpt);
+    CHECK(r.cache.peek_prefix({1, 11, 12}).matched_tokens == 0);
+    CHECK(r.tier.pool().used == 6 * kBpt);
+    CHECK(engine().free_tokens(KVF_TIER_DEVICE) == free0 - 6);
+    r.tier.audit(r.cache);
+}
+
+TEST("evict: match refreshes recency, peek does not") {
+    for (bool use_match : {false, true}) {
+        Rig r;
+        r.put({1, 11}, 1.0);
+        r.put({2, 22}, 2.0);
+        if (use_match) CHECK(r.cache.match_prefix({1, 11}, 4.0).matched_tokens == 2);
+        else CHECK(r.cache.peek_prefix({1, 11}).matched_tokens == 2);
+        EvictOutcome out = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 5.0);
+        REQUIRE(out.victims.size() == 1);
+        CHECK(out.victims[0].node_id == r.id_of(use_match ? TokenSeq{2, 22} : TokenSeq{1, 11}));
+    }
+}
+
+TEST("evict: workflow-aware order (suffix, then larger steps) and the rank floor") {
+    for (bool floor : {false, true}) {
+        Rig r;
+        r.put({1, 11, 12}, 1.0);
+        r.put({2, 21, 22}, 2.0);
+        r.put({3, 31, 32}, 3.0);
+        AgentId a{0, "a"}, b{0, "b"};
+        r.cache.mark_fixed_boundary(a, {1, 11, 12}, 3);
+        r.cache.mark_fixed_boundary(b, {2, 21, 22}, 3);
+        StepMap steps;
+        steps[a] = 5;
+        steps[b] = 1;
+        r.cache.set_agent_priorities(steps);  // K4
+        EvictRequest req{floor ? Bytes(1 << 20) : 9 * kBpt, EvictionPolicy::WorkflowAware, TierMode::Discard, {}};
+        if (floor) req.rank_floor_exclusive = rank_for_step(1);
+        EvictOutcome out = r.cache.evict(req, r.tier, 4.0);  // K5
+        REQUIRE(out.victims.size() == (floor ? 2u : 3u));
+        CHECK(out.victims[0].node_id == r.id_of({3, 31, 32}));
+        CHECK(out.victims[1].node_id == r.id_of({1, 11, 12}));
+        if (!floor) CHECK(out.victims[2].node_id == r.id_of({2, 21, 22}));
+        CHECK(out.sufficient == !floor);
+        if (floor) CHECK(r.cache.peek_prefix({2, 21, 22}).matched_tokens == 3);
+    }
+}
+
+TEST("evict: leaves before parents, a freed parent follows in the same pass; locks protect") {
+    {
+        Rig r;
+        r.put({1, 2}, 1.0);
+        r.put({1, 2, 3}, 2.0);
+        const uint64_t p = r.id_of({1, 2}), l = r.id_of({3});
+        EvictOutcome out = r.cache.evict({3 * kBpt, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 3.0);
+        REQUIRE(out.victims.size() == 2);
+        CHECK(out.victims[0].node_id == l);
+        CHECK(out.victims[1].node_id == p);
+        CHECK(r.cache.node_count() == 0);
+    }
+    {
+        Rig r;
+        InsertResult a = r.put({1, 11}, 1.0);
+        r.put({2, 22}, 2.0);
+        r.cache.lock_root_path(a.path.back());
+        EvictOutcome out = r.cache.evict({1 << 20, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 3.0);
+        REQUIRE(out.victims.size() == 1);
+        CHECK(out.victims[0].node_id == r.id_of({2, 22}));
+        CHECK(!out.sufficient);
+        r.cache.unlock_root_path(a.path.back());
+    }
+}
+
+TEST("offload eviction moves real bytes; a backed copy makes the next eviction instant") {
+    Rig r;
+    r.put({1, 11, 12}, 1.0);
+    CacheNode* n = r.node({1, 11, 12});
+    REQUIRE(r.dev_ok(*n));
+    EvictOutcome out = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, 2.0);
+    REQUIRE(out.victims.size() == 1);
+    CHECK(!out.victims[0].immediate);
+    CHECK(n->status == NodeStatus::Offloading);
+    Event done = r.ev.pop();
+    r.tier.complete(done.id, done.time);  // K2 fence
+    CHECK(n->status == NodeStatus::BackupInCpu);
+    CHECK(n->dev_runs.empty());
+    CHECK(r.host_ok(*n));
+    r.tier.audit(r.cache);
+    r.tier.begin_load(*n, done.time, 3 * kBpt, TransferPurpose::Reactive);
+    Event loaded = r.ev.pop();
+    r.tier.complete(loaded.id, loaded.time);  // K1 fence
+    CHECK(n->status == NodeStatus::InGpu);
+    CHECK(r.dev_ok(*n));
+    EvictOutcome again = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, loaded.time + 1);
+    REQUIRE(again.victims.size() == 1);
+    CHECK(again.victims[0].immediate);
+    CHECK(n->status == NodeStatus::BackupInCpu);
+    CHECK(r.ev.empty());
+    r.tier.audit(r.cache);
+}
+
+TEST("a full backup tier falls back to plain discard") {
+    Rig r(3 * kBpt);
+    r.put({1, 11, 12}, 1.0);
+    r.put({2, 21, 22}, 2.0);
+    EvictOutcome first = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, 3.0);
+    REQUIRE(first.victims.size() == 1);
+    Event done = r.ev.pop();
+    r.tier.complete(done.id, done.time);
+    CHECK(r.tier.cpu_used() == 3 * kBpt);
+    EvictOutcome second = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, 4.0);
+    REQUIRE(second.victims.size() == 1);
+    CHECK(second.victims[0].immediate);
+    CHECK(r.cache.peek_prefix({2, 21, 22}).matched_tokens == 0);
+    CHECK(r.ev.empty());
+    r.tier.audit(r.cache);
+}
+
+TEST("dump renders priorities deterministically (reference golden string)") {
+    Rig r;
+    r.cache.insert({1, 2, 3, 4}, 1.0);
+    r.cache.insert({1, 2, 5}, 2.0);
+    r.cache.insert({7}, 3.0);
+    AgentId w{0, "writer"};
+    r.cache.mark_fixed_boundary(w, {1, 2, 5}, 3);
+    StepMap s;
+    s[w] = 2;
+    r.cache.set_agent_priorities(s);
+    CHECK(r.cache.dump() ==
+          "root\n"
+          "  [1..+1] IN_GPU STEP(2) lock=0\n"
+          "    [3..+1] IN_GPU SUFFIX lock=0\n"
+          "    [5] IN_GPU STEP(2) lock=0 boundary{c0/writer}\n"
+          "  [7] IN_GPU SUFFIX lock=0\n");
+}
+
+TEST("K4 priorities equal brute force on random trees; splits keep every node's bytes") {
+    std::mt19937_64 rng(20260822);
+    for (int t = 0; t < 60; ++t) {
+        Rig r;
+        std::vector<TokenSeq> used;
+        VirtualTime now = 0;
+        for (int i = 0, e = 5 + static_cast<int>(rng() % 21); i < e; ++i) {
+            TokenSeq s;
+            if (!used.empty() && rng() % 2) {
+                const TokenSeq& b = used[rng() % used.size()];
+                s.assign(b.begin(), b.begin() + static_cast<long>(1 + rng() % b.size()));
+            }
+            for (int k = 0, m = 4 + static_cast<int>(rng() % 17); k < m; ++k) s.push_back(static_cast<TokenId>(rng() % 4));
+            r.put(s, now += 1.0);
+            used.push_back(s);
+        }
+        std::vector<std::pair<AgentId, std::pair<TokenSeq, size_t>>> marks;
+        for (size_t a = 0, na = 1 + rng() % 6; a < na; ++a) {
+            AgentId id{static_cast<ClientId>(rng() % 2), "agent" + std::to_string(a)};
+            const TokenSeq& s = used[rng() % used.size()];
+            size_t fl = 1 + rng() % s.size();
+            r.cache.mark_fixed_boundary(id, s, fl);
+            marks.push_back({id, {s, fl}});
+        }
+        StepMap steps;
+        for (auto& m : marks) {
+            uint64_t x = rng() % 10;
+            if (x < 7) steps[m.first] = static_cast<StepValue>(rng() % 9);
+            else if (x == 7) steps[m.first] = kStepUnreachable;
+        }
+        r.cache.set_agent_priorities(steps);
+        std::map<const CacheNode*, int64_t> want;
+        r.cache.for_each_node([&](const CacheNode& n) { want[&n] = kRankSuffix; });
+        for (auto& m : marks) {
+            CacheNode* b = r.cache.boundary_node(m.first);
+            REQUIRE(b != nullptr);
+            auto it = steps.find(m.first);
+            int64_t v = rank_for_step(it == steps.end() ? kStepUnreachable : it->second);
+            for (CacheNode* n = b; n && !n->is_root(); n = n->parent) want[n] = std::min(want[n], v);
+        }
+        r.cache.for_each_node([&](const CacheNode& n) {
+            CHECK(n.rank == want[&n]);
+            CHECK(r.dev_ok(n));
+        });
+    }
+}
+
+TEST("tier manager with bytes: FIFO jobs, fences, write-once host copies, audit") {
+    Rig r;
+    r.put({1, 2, 3, 4, 5, 6, 7, 8}, 0.0);
+    r.put({9, 10, 11}, 0.0);
+    CacheNode* a = r.node({1, 2, 3, 4, 5, 6, 7, 8});
+    CacheNode* b = r.node({9, 10, 11});
+    r.tier.begin_offload(*a, 1.0, r.cache.node_bytes(*a));
+    r.tier.begin_offload(*b, 1.0, r.cache.node_bytes(*b));
+    CHECK(r.tier.inflight_count() == 2);
+    while (!r.ev.empty()) {
+        Event e = r.ev.pop();
+        const TransferJob& j = r.tier.complete(e.id, e.time);
+        CHECK(j.device_ms >= 0.0f);
+    }
+    CHECK(r.host_ok(*a));
+    CHECK(r.host_ok(*b));
+    const RunList host_before = a->host_runs;
+    r.tier.begin_load(*a, 2.0, r.cache.node_bytes(*a), TransferPurpose::Prefetch, AgentId{1, "x"});
+    Event e = r.ev.pop();
+    r.tier.complete(e.id, e.time);
+    CHECK(a->prefetched_unused);
+    CHECK(r.dev_ok(*a));
+    r.tier.begin_offload(*a, 3.0, r.cache.node_bytes(*a));  // re-offload: same host slots
+    Event e2 = r.ev.pop();
+    r.tier.complete(e2.id, e2.time);
+    CHECK(a->host_runs.size() == host_before.size() && a->host_runs[0].start == host_before[0].start);
+    CHECK(r.tier.cpu_used() == (8 + 3) * kBpt);
+    CHECK(r.host_ok(*a));
+    r.tier.audit(r.cache);
+    // split of a backed node splits both run lists; bytes stay put and stay correct
+    r.tier.begin_load(*a, 4.0, r.cache.node_bytes(*a), TransferPurpose::Reactive);
+    Event e3 = r.ev.pop();
+    r.tier.complete(e3.id, e3.time);
+    r.put({1, 2, 3, 99}, 5.0);
+    CacheNode* up = r.node({1, 2, 3});
+    REQUIRE(up != nullptr);
+    CHECK(r.dev_ok(*up) && r.dev_ok(*a) && r.host_ok(*up) && r.host_ok(*a));
+    r.tier.audit(r.cache);
+}
+
+TT_MAIN
