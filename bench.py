@@ -133,17 +133,16 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
-    heads = 8 // world
-    assert heads * world == 8, "KV-head sharding needs N | 8"
-    bpt, budget = BPT_FULL // world, BUDGET_FULL // world
+    from paper_2507_07400_b200.shard import plan
+    sp = plan(rank, world, layers=32, kv_heads=8, head_dim=128, gpu_budget=BUDGET_FULL)
+    heads, bpt, budget = sp.kv_heads_local, sp.bytes_per_token, sp.gpu_budget
     gpu_slots = budget // bpt
     suffix = DYN + OUT
     peaks, peak_src = measured_peaks()
     pcie = ce_h2d_peak(torch)
 
     # ---- kernel-level steady-state replay (value, roofline) --------------------------
-    eng = Engine(layers=32, kv_heads_total=8, kv_heads_local=heads, head_offset=rank * heads, head_dim=128,
-                 gpu_slots=gpu_slots, host_slots=4 * FIXED + 64 * suffix, device=local)
+    eng = Engine(**sp.engine_kwargs(), gpu_slots=gpu_slots, host_slots=4 * FIXED + 64 * suffix, device=local)
     rng = np.random.default_rng(1)
     fixed_host = [eng.alloc(N.KVF_TIER_HOST, FIXED) for _ in range(4)]
     for r in fixed_host:
@@ -194,8 +193,7 @@ def run_ours(args, rank, world, local):
     eng.close()
 
     # ---- e2e: the full workflow through the public API ---------------------------------
-    sim = Sim(fixed=FIXED, dyn=DYN, out=OUT, gpu_cap=budget, bytes_per_token=bpt, layers=32, kv_heads_total=8,
-              kv_heads_local=heads, head_offset=rank * heads, head_dim=128, device=local)
+    sim = Sim(fixed=FIXED, dyn=DYN, out=OUT, gpu_cap=budget, bytes_per_token=bpt, device=local, **sp.engine_kwargs())
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()

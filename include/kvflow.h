@@ -196,6 +196,7 @@ typedef struct {
     uint64_t h2d_jobs, d2h_jobs, dev_jobs, decisions;
     double decision_kernel_ms; /* K4+K5 kernel time, CUDA events on the decision stream */
     double decision_call_us;   /* K4+K5 host round trip (pack, H2D, kernel, D2H, sync)  */
+    double k5_phase_ns[5];     /* K5 in-kernel phases: stage, sort, walks, victim sort, scan+out */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

@@ -60,7 +60,7 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("dev_bytes", C.c_uint64), ("h2d_jobs", C.c_uint64), ("d2h_jobs", C.c_uint64),
                 ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
-                ("decision_call_us", C.c_double)]
+                ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature

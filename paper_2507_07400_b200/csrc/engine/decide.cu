@@ -29,7 +29,8 @@ using namespace kvf_impl;
 
 namespace {
 
-constexpr int64_t kRankSuffix = INT64_MAX / 2;
+constexpr int64_t kRankSuffix = INT64_MAX / 2;        // radix_cache.hpp:30-38
+constexpr int64_t kRankUnreachable = INT64_MAX / 4;
 constexpr uint32_t kMaxNodesSingleCta = 4096;
 constexpr int kThreads = 1024;
 constexpr int32_t kBlocked = INT32_MAX;
@@ -74,22 +75,16 @@ struct OutDev {
     unsigned long long* header;  // [count, immediate, pending]
 };
 
-__device__ __forceinline__ void bitonic_u64(uint64_t* a, uint32_t P) {
-    for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                const uint32_t l = i ^ j;
-                if (l > i) {
-                    const bool up = (i & k) == 0;
-                    const uint64_t x = a[i], y = a[l];
-                    if ((y < x) == up) {
-                        a[i] = y;
-                        a[l] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
+// Warp-aggregated slot claim on a shared counter: one atomic per warp instead of per lane.
+__device__ __forceinline__ uint32_t claim(uint32_t* counter, bool take) {
+    const unsigned act = __activemask();
+    const unsigned mask = __ballot_sync(act, take);
+    const uint32_t lane = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    uint32_t base = 0;
+    if (static_cast<int>(lane) == leader && mask) base = atomicAdd(counter, static_cast<uint32_t>(__popc(mask)));
+    base = __shfl_sync(act, base, leader);
+    return base + __popc(mask & ((1u << lane) - 1u));
 }
 
 __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
@@ -98,85 +93,150 @@ __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
     return p;
 }
 
+// Bitonic sort over P (power of two) elements with one compare-exchange per pair index.
+// Pair p -> (i, i|j) with i = insert-zero-bit(p, log2 j).  Each warp owns a 32-aligned range
+// of pair indices, so stages with j <= 32 touch only that warp's 64-element chunk and need
+// just __syncwarp; only j >= 64 stages pay a block barrier (15 of 66 stages at P = 2048).
+template <typename Greater, typename Swap>
+__device__ __forceinline__ void bitonic(uint32_t P, Greater greater, Swap swap) {
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 64) __syncthreads();
+            for (uint32_t pr = threadIdx.x; pr < P / 2; pr += blockDim.x) {
+                const uint32_t i = ((pr & ~(j - 1)) << 1) | (pr & (j - 1));
+                const uint32_t l = i | j;
+                const bool up = (i & k) == 0;
+                if (up ? greater(i, l) : greater(l, i)) swap(i, l);
+            }
+            if (j >= 64) __syncthreads();
+            else __syncwarp();
+        }
+    __syncthreads();
+}
+
+// Order-preserving u64 image of a double (-0.0 == +0.0 as in the reference's `!=`).
+__device__ __forceinline__ uint64_t time_order(double t) {
+    const uint64_t b = t == 0.0 ? 0ull : static_cast<uint64_t>(__double_as_longlong(t));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 // Shared-memory layout for n <= 4096 nodes (PN = pow2 >= n):
-//   region A (32*PN B): phase-1 sort keys time|seq|id|rank per node, later reused for the
-//                       final 64-bit victim keys and the byte prefix
-//   region B:           parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | sel u16[PN]
-//                       | status u8[n] | flags u8[n]
+//   pk0 u64[PN] | pk1 u64[PN]   phase-1 primary keys by position (later: final keys | prefix)
+//   parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | sel u16[PN] | status u8[n] | flags u8[n]
 // flags: bit0 selfok, bit1 releases, bit2 R
 __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, const ReqDev q, OutDev o) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t n = t.n;
     const uint32_t PN = pow2_ceil(n > 1 ? n : 2);
-    double* k_time = reinterpret_cast<double*>(sm);
-    uint64_t* k_seq = reinterpret_cast<uint64_t*>(k_time + PN);
-    uint64_t* k_id = k_seq + PN;
-    int64_t* k_rank = reinterpret_cast<int64_t*>(k_id + PN);
-    uint64_t* keys = reinterpret_cast<uint64_t*>(sm);  // phase 3 reuse of region A
-    uint64_t* pref = keys + PN;
-    int32_t* parent = reinterpret_cast<int32_t*>(k_rank + PN);
+    uint64_t* pk0 = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* pk1 = pk0 + PN;
+    uint64_t* keys = pk0;  // reuse after phase 1
+    uint64_t* pref = pk1;
+    int32_t* parent = reinterpret_cast<int32_t*>(pk1 + PN);
     int32_t* ord = parent + n;
     int32_t* eff = ord + n;
     uint32_t* blocked = reinterpret_cast<uint32_t*>(eff + n);
     uint16_t* sel = reinterpret_cast<uint16_t*>(blocked + n);
     uint8_t* st = reinterpret_cast<uint8_t*>(sel + PN);
     uint8_t* flags = st + n;
-    __shared__ uint32_t s_cnt, s_rcnt;
-    __shared__ unsigned long long s_imm, s_pend, s_warp[kThreads / 32];
+    __shared__ uint32_t s_cnt, s_rcnt, s_slow;
+    __shared__ unsigned long long s_imm, s_pend, s_warp[32];
+    // per-phase timestamps (globaltimer ns) -> header[3..10], read by kvf_get_stats
+    auto stamp = [&](int k) {
+        if (threadIdx.x == 0) {
+            unsigned long long t_ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns));
+            o.header[3 + k] = t_ns;
+        }
+    };
+    stamp(0);
     if (threadIdx.x == 0) {
-        s_cnt = 0;
-        s_rcnt = 0;
-        s_imm = 0;
-        s_pend = 0;
+        s_cnt = s_rcnt = s_slow = 0;
+        s_imm = s_pend = 0;
     }
     __syncthreads();
     const bool wa = q.wa != 0;
     // 1. stage the snapshot; self-eligibility (radix_cache.cpp:305-312 minus the device-child
-    //    test) and whether evicting the node frees its parent (Discard / backed / CPU full)
+    //    test); whether evicting a node frees its parent (Discard / backed / CPU full)
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint8_t s = t.status[i];
         const uint64_t bytes = t.tokens[i] * t.bpt;
         const bool cpu_room = q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap;
-        const bool selfok = i > 0 && t.lock[i] == 0 && s == 0 && (!q.has_floor || t.rank[i] > q.floor);
+        const int64_t rank = t.rank[i];
+        const bool selfok = i > 0 && t.lock[i] == 0 && s == 0 && (!q.has_floor || rank > q.floor);
         const bool releases = !q.offload || t.backed[i] || !cpu_room;
         parent[i] = t.parent[i];
         st[i] = s;
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
         blocked[i] = 0;
         ord[i] = -1;
-        k_time[i] = t.time[i];
-        k_seq[i] = t.seq[i];
-        k_id[i] = t.id[i];
-        k_rank[i] = t.rank[i];
-        if (selfok) sel[atomicAdd(&s_cnt, 1u)] = static_cast<uint16_t>(i);
+        const uint32_t k = claim(&s_cnt, selfok);
+        if (selfok) {
+            sel[k] = static_cast<uint16_t>(i);
+            // primary key: an exact coarsening of `before` (radix_cache.cpp:316-321) when ranks fit
+            // 16 bits and seq fits 48; ties fall back to the full comparison
+            const uint64_t tord = time_order(t.time[i]);
+            const uint64_t seq = t.seq[i];
+            if (wa) {
+                uint64_t code;
+                if (rank == kRankSuffix) code = 0;
+                else if (rank == kRankUnreachable) code = 1;
+                else if (rank >= 0 && rank <= 0xFFFD) code = 0xFFFFull - static_cast<uint64_t>(rank);
+                else { code = 0xFFFF; atomicOr(&s_slow, 1u); }
+                if (seq >> 48) atomicOr(&s_slow, 1u);
+                pk0[k] = (code << 48) | (tord >> 16);
+                pk1[k] = (tord << 48) | (seq & 0xFFFFFFFFFFFFull);
+            } else {
+                pk0[k] = tord;
+                pk1[k] = seq;
+            }
+        }
     }
     __syncthreads();
     const uint32_t c = s_cnt;
     const uint32_t P = pow2_ceil(c > 1 ? c : 2);
-    for (uint32_t i = c + threadIdx.x; i < P; i += blockDim.x) sel[i] = 0xFFFFu;
-    __syncthreads();
-    // 2. candidates in `before` order (radix_cache.cpp:316-321) -> ord
-    for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-                const uint32_t l = i ^ j;
-                if (l <= i) continue;
-                const uint32_t x = sel[i], y = sel[l];
-                bool y_first;
-                if (x == 0xFFFFu) y_first = y != 0xFFFFu;
-                else if (y == 0xFFFFu) y_first = false;
-                else if (wa && k_rank[x] != k_rank[y]) y_first = k_rank[y] > k_rank[x];
-                else if (k_time[x] != k_time[y]) y_first = k_time[y] < k_time[x];
-                else if (k_seq[x] != k_seq[y]) y_first = k_seq[y] < k_seq[x];
-                else y_first = k_id[y] < k_id[x];
-                if (y_first == ((i & k) == 0)) {
-                    sel[i] = static_cast<uint16_t>(y);
-                    sel[l] = static_cast<uint16_t>(x);
-                }
-            }
-            __syncthreads();
+    for (uint32_t i = c + threadIdx.x; i < P; i += blockDim.x) {
+        sel[i] = 0xFFFFu;
+        pk0[i] = pk1[i] = ~0ull;
+    }
+    const bool slow = s_slow != 0;
+    stamp(1);
+    // 2. candidates in `before` order -> ord
+    auto full_after = [&](uint32_t x, uint32_t y) {  // is node x after node y?
+        if (wa) {
+            const int64_t rx = __ldg(t.rank + x), ry = __ldg(t.rank + y);
+            if (rx != ry) return rx < ry;
         }
+        const double tx = __ldg(t.time + x), ty = __ldg(t.time + y);
+        if (tx != ty) return tx > ty;
+        const uint64_t sx = __ldg(t.seq + x), sy = __ldg(t.seq + y);
+        if (sx != sy) return sx > sy;
+        return __ldg(t.id + x) > __ldg(t.id + y);
+    };
+    bitonic(
+        P,
+        [&](uint32_t a, uint32_t b) {  // element at a must come after element at b
+            const uint32_t x = sel[a], y = sel[b];
+            if (x == 0xFFFFu || y == 0xFFFFu) return x == 0xFFFFu && y != 0xFFFFu;
+            if (!slow) {
+                if (pk0[a] != pk0[b]) return pk0[a] > pk0[b];
+                if (pk1[a] != pk1[b]) return pk1[a] > pk1[b];
+            }
+            return full_after(x, y);
+        },
+        [&](uint32_t a, uint32_t b) {
+            const uint16_t s0 = sel[a];
+            sel[a] = sel[b];
+            sel[b] = s0;
+            const uint64_t p0 = pk0[a], p1 = pk1[a];
+            pk0[a] = pk0[b];
+            pk1[a] = pk1[b];
+            pk0[b] = p0;
+            pk1[b] = p1;
+        });
     for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) ord[sel[k]] = static_cast<int32_t>(k);
+    stamp(2);
     // 3. blocked(n): some node of n's device subtree (below n) is not self-eligible or would
     //    not release it (has_device_child, radix_cache.cpp:40-45).  Every such node walks up
     //    through device-child links; a walker stops where another already passed.
@@ -211,24 +271,33 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
         }
     }
     __syncthreads();
+    stamp(3);
     // 5. victims = R sorted by (eff asc, depth desc); keys are unique per node
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-        if (flags[i] & 4)
-            keys[atomicAdd(&s_rcnt, 1u)] = (static_cast<uint64_t>(eff[i]) << 32) |
-                                            (static_cast<uint64_t>(0xFFFFu - t.depth[i]) << 16) | i;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const bool r_node = (flags[i] & 4) != 0;
+        const uint32_t k = claim(&s_rcnt, r_node);
+        if (r_node)
+            keys[k] = (static_cast<uint64_t>(eff[i]) << 32) | (static_cast<uint64_t>(0xFFFFu - t.depth[i]) << 16) | i;
+    }
     __syncthreads();
     const uint32_t r = s_rcnt;
     const uint32_t PR = pow2_ceil(r > 1 ? r : 2);
     for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
-    __syncthreads();
-    bitonic_u64(keys, PR);
-    // 6. exclusive byte prefix in victim order (block scan, <= 4 items per thread)
+    bitonic(
+        PR, [&](uint32_t a, uint32_t b) { return keys[a] > keys[b]; },
+        [&](uint32_t a, uint32_t b) {
+            const uint64_t x = keys[a];
+            keys[a] = keys[b];
+            keys[b] = x;
+        });
+    stamp(4);
+    // 6. exclusive byte prefix in victim order (block scan)
     const uint32_t per = (r + blockDim.x - 1) / blockDim.x;
     const uint32_t lo_k = threadIdx.x * per, hi_k = min(r, (threadIdx.x + 1) * per);
     uint64_t local = 0;
     for (uint32_t k = lo_k; k < hi_k; ++k) local += t.tokens[keys[k] & 0xFFFFu] * t.bpt;
     uint64_t inc = local;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int off = 1; off < 32; off <<= 1) {
         const uint64_t y = __shfl_up_sync(0xffffffffu, inc, off);
         if (lane >= off) inc += y;
@@ -236,16 +305,17 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        uint64_t w = lane < blockDim.x / 32 ? s_warp[lane] : 0;
+        uint64_t w = lane < nwarps ? s_warp[lane] : 0;
         for (int off = 1; off < 32; off <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, w, off);
             if (lane >= off) w += y;
         }
-        if (lane < blockDim.x / 32) s_warp[lane] = w;
+        if (lane < nwarps) s_warp[lane] = w;
     }
     __syncthreads();
     uint64_t run = inc - local + (warp ? s_warp[warp - 1] : 0);
     // 7. victim k is popped iff the bytes freed before it are still < needed (radix_cache.cpp:335)
+    uint64_t my_imm = 0, my_pend = 0;
     for (uint32_t k = lo_k; k < hi_k; ++k) {
         const uint32_t v = static_cast<uint32_t>(keys[k] & 0xFFFFu);
         const uint64_t bytes = t.tokens[v] * t.bpt;
@@ -257,13 +327,20 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
             else act = KVF_ACT_OFFLOAD;
             o.idx[k] = static_cast<int32_t>(v);
             o.action[k] = act;
-            if (act == KVF_ACT_OFFLOAD) atomicAdd(&s_pend, static_cast<unsigned long long>(bytes));
-            else atomicAdd(&s_imm, static_cast<unsigned long long>(bytes));
+            (act == KVF_ACT_OFFLOAD ? my_pend : my_imm) += bytes;
             pref[k] = 1;
         } else {
             pref[k] = 0;
         }
         run += bytes;
+    }
+    for (int off = 16; off; off >>= 1) {  // one shared atomic per warp
+        my_imm += __shfl_xor_sync(0xffffffffu, my_imm, off);
+        my_pend += __shfl_xor_sync(0xffffffffu, my_pend, off);
+    }
+    if (lane == 0) {
+        if (my_imm) atomicAdd(&s_imm, static_cast<unsigned long long>(my_imm));
+        if (my_pend) atomicAdd(&s_pend, static_cast<unsigned long long>(my_pend));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -276,11 +353,17 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
         o.header[1] = s_imm;
         o.header[2] = s_pend;
     }
+    stamp(5);
 }
 
 size_t victim_smem(uint32_t n) {
     const size_t PN = pow2_ceil(n > 1 ? n : 2);
-    return PN * 32 + static_cast<size_t>(n) * 16 + PN * 2 + 2 * ((n + 15) & ~15u) + 64;
+    return PN * 16 + static_cast<size_t>(n) * 16 + PN * 2 + 2 * ((n + 15) & ~15u) + 64;
+}
+
+uint32_t victim_threads(uint32_t n) {  // one compare-exchange per thread per sort stage
+    const uint32_t half = pow2_ceil(n > 1 ? n : 2) / 2;
+    return half < 32 ? 32 : (half > static_cast<uint32_t>(kThreads) ? kThreads : half);
 }
 
 int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
@@ -404,7 +487,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
         attr = victim_smem(kMaxNodesSingleCta);
     }
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
-    kvf_victim_kernel<<<1, kThreads, smem, e->s_dec>>>(td, rq, od);
+    kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od);
     KVF_CUDA(cudaGetLastError());
     KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
@@ -414,6 +497,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
+    for (int k = 0; k < 5; ++k) e->stats.k5_phase_ns[k] += static_cast<double>(hdr[4 + k] - hdr[3 + k]);
     std::memcpy(out_idx, hout + 64, cnt * 4);
     std::memcpy(out_action, hout + 64 + ((n * 4 + 15) & ~15ull), cnt);
     *out_count = cnt;

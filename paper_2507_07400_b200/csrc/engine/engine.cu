@@ -716,6 +716,10 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
         return fail(cuda_error(err, "cudaEventCreate"));
     if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_checksum), sizeof(uint64_t))) != cudaSuccess)
         return fail(cuda_error(err, "cudaMalloc(checksum)"));
+    // Size the staging workspaces once: growing them later means cudaFree (a device-wide
+    // sync) and cudaHostAlloc inside a decision call -- milliseconds on the hot path.
+    if (int rc = e->ws_dec.ensure(1u << 20, 1u << 20)) return fail(rc);
+    if (int rc = e->ws_dev.ensure(4u << 20, 4u << 20)) return fail(rc);
     *out = e;
     return KVF_OK;
 }

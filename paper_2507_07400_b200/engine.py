@@ -158,7 +158,7 @@ class Engine:
     def stats(self):
         s = N.Stats()
         N.check(self._lib.kvf_get_stats(self.h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in N.Stats._fields_}
+        return {f: (list(getattr(s, f)) if f == "k5_phase_ns" else getattr(s, f)) for f, _ in N.Stats._fields_}
 
     # ---- decisions ---------------------------------------------------------------------
     def priority(self, parent, bidx, cand):

@@ -56,6 +56,7 @@ def main():
             row[f"k5_kernel_us_{key}"] = round((s1["decision_kernel_ms"] - s0["decision_kernel_ms"]) / reps * 1e3, 2)
             row[f"k5_call_us_{key}"] = round((s1["decision_call_us"] - s0["decision_call_us"]) / reps, 2)
             row[f"k5_python_us_{key}"] = round(wall, 2)
+            row[f"k5_phase_us_{key}"] = [round((b - a) / reps / 1e3, 2) for a, b in zip(s0["k5_phase_ns"], s1["k5_phase_ns"])]
         w0 = time.perf_counter()
         for _ in range(reps):
             oracle_evict(c)
