@@ -19,7 +19,9 @@ namespace {
 constexpr Bytes kBpt = 16;  // 1 layer x 1 head x 4 dims x bf16 x {K,V}
 
 Engine& engine() {
-    static Engine e([] {
+    // intentionally leaked: a static Engine would be destroyed after the CUDA runtime's own
+    // atexit teardown
+    static Engine& e = *new Engine([] {
         EngineOptions o;
         o.layers = 1;
         o.kv_heads_total = 1;

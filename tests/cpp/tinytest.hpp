@@ -53,6 +53,7 @@ inline int run_all(int argc, char** argv) {
         const bool ok = failures() == before;
         if (!ok) ++bad;
         std::printf("[%s] %s\n", ok ? " ok " : "FAIL", c.name);
+        std::fflush(stdout);
     }
     std::printf("%d/%d test cases passed\n", ran - bad, ran);
     return bad;

@@ -24,6 +24,9 @@ G="$HERE"
 "$T" sim fixed=8192 gpu_cap=3271557120 > "$G/sim_c2.jsonl"
 # C4 64 workflows, intra-client shared prefixes, 16 GiB budget
 "$T" sim fixed=1024 shared_prefix=512 dyn=256 out=256 workflows=64 iterations=4 gpu_cap=17179869184 dump=0 > "$G/sim_c4.jsonl"
+# C4 as one of 8 KV-head shards (16 KiB/token, 2 GiB budget); every shard runs this stream
+# (it differs from G=1: transfers are 8x shorter while compute is not, so events reorder)
+"$T" sim fixed=1024 shared_prefix=512 dyn=256 out=256 workflows=64 iterations=4 gpu_cap=2147483648 bpt=16384 dump=0 > "$G/sim_c4_g8.jsonl"
 # C5 Llama-3-70B KV head-sharded: per-shard bytes/token and budget divide by G
 for G_ in 1 2 4 8; do
   "$T" sim fixed=2048 bpt=$((327680 / G_)) gpu_cap=$((2139095040 / G_)) > "$G/sim_c5_g${G_}.jsonl"
@@ -43,4 +46,8 @@ done
 "$T" sim $M topology=BRANCH_MIN agents=4 iterations=3 warmup=1 fixed=128 dyn=16 out=8 workflows=2 gpu_cap=9000 seed=12 audit=1 > "$G/sim_m_branch_min.jsonl"
 "$T" sim $M topology=PEER_STYLE agents=4 iterations=2 warmup=1 workflows=3 gpu_cap=40000 seed=13 audit=1 > "$G/sim_m_peer_style.jsonl"
 "$T" sim $M topology=CYCLIC agents=4 iterations=3 warmup=1 fixed=96 dyn=8 out=8 workflows=3 shared_prefix=32 gpu_cap=9000 seed=14 audit=1 > "$G/sim_m_shared.jsonl"
+# C3: 16-agent branch + barrier graph, mixed 1k-8k prompts (component-level harness,
+# tests/cpp/c3_harness.hpp); one Llama-3-8B KV head (16 KiB/token), 24k-token budget
+"$ROOT/oracle/_ref/ref_c3" 3 4 16384 393216000 > "$G/c3_seed3.jsonl"
+"$ROOT/oracle/_ref/ref_c3" 11 6 16384 262144000 > "$G/c3_seed11.jsonl"
 echo "golden fixtures regenerated in $G"
