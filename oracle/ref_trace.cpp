@@ -259,8 +259,10 @@ struct Scenario {
 };
 
 void grow(Scenario& sc, std::mt19937_64& rng, size_t target_nodes, int vocab, VirtualTime& now) {
-    size_t guard = 0;
-    while (sc.cache.node_count() < target_nodes && guard++ < target_nodes * 8) {
+    size_t guard = 0, count = sc.cache.node_count();
+    while (count < target_nodes && guard++ < target_nodes * 8) {
+        if (guard % 64 == 0) count = sc.cache.node_count();  // O(n): not every insert
+        else count += 2;                                      // an insert adds <= 2 nodes
         TokenSeq s = rand_seq(rng, sc.seqs, vocab, 1, 12);
         InsertResult ins = sc.cache.insert(s, now += static_cast<double>(rng() % 3));  // equal times happen
         sc.tier.reserve_working(ins.new_bytes);
@@ -370,7 +372,10 @@ int run_evict(const std::map<std::string, std::string>& kv) {
                     req.rank_floor_exclusive ? 1 : 0, req.rank_floor_exclusive.value_or(0), cpu_used, sc.tier.cpu_capacity());
         (void)cpu_cap;
         try {
+            auto t0 = std::chrono::steady_clock::now();
             EvictOutcome out = sc.cache.evict(req, sc.tier, now + 1.0);
+            const double evict_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+            std::printf(",\"evict_us\":%.3f", evict_us);
             std::string v;
             for (size_t i = 0; i < out.victims.size(); ++i) {
                 const auto& x = out.victims[i];
@@ -430,7 +435,10 @@ int run_evict_bounded(const std::map<std::string, std::string>& kv) {
                     ",\"cpu_cap\":%" PRIu64,
                     req.needed, req.policy == EvictionPolicy::WorkflowAware ? 1 : 0, sc.tier.cpu_used(), sc.tier.cpu_capacity());
         try {
+            auto t0 = std::chrono::steady_clock::now();
             EvictOutcome out = sc.cache.evict(req, sc.tier, now + 1.0);
+            const double evict_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+            std::printf(",\"evict_us\":%.3f", evict_us);
             std::string v;
             for (size_t i = 0; i < out.victims.size(); ++i) {
                 const auto& x = out.victims[i];

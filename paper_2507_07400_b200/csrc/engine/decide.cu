@@ -34,6 +34,8 @@ constexpr int64_t kRankUnreachable = INT64_MAX / 4;
 constexpr uint32_t kMaxNodesSingleCta = 4096;
 constexpr int kThreads = 1024;
 constexpr int32_t kBlocked = INT32_MAX;
+// K5 result header: [count, immediate, pending, phase stamps x6] -> 9 words, padded
+constexpr size_t kHeaderBytes = 128;
 
 __global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* __restrict__ parent, uint32_t n,
                                                                 const int32_t* __restrict__ bidx,
@@ -72,7 +74,7 @@ struct ReqDev {
 struct OutDev {
     int32_t* idx;
     uint8_t* action;
-    unsigned long long* header;  // [count, immediate, pending]
+    unsigned long long* header;  // [count, immediate, pending, 6 phase stamps] (kHeaderBytes)
 };
 
 // Warp-aggregated slot claim on a shared counter: one atomic per warp instead of per lane.
@@ -435,13 +437,15 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     *out_count = 0;
     *out_imm = *out_pend = 0;
     if (n <= 1 || q->needed == 0) return KVF_OK;
-    if (n > kMaxNodesSingleCta)
-        return set_error(KVF_E_TOO_LARGE, "victim selection above 4096 nodes needs the multi-CTA path");
     const auto t0 = std::chrono::steady_clock::now();
+    if (n > kMaxNodesSingleCta) {  // device-wide path (decide_large.cu)
+        int rc = victim_select_large(e, t, q, out_idx, out_action, out_count, out_imm, out_pend);
+        return rc ? rc : finish_decision(e, t0);
+    }
     // pack the SoA snapshot into one pinned buffer -> one H2D copy
     const size_t in_bytes = 5 * ((n * 8 + 15) & ~15ull) + 2 * ((n * 4 + 15) & ~15ull) + ((n * 2 + 15) & ~15ull) +
                             2 * ((n + 15) & ~15ull);
-    const size_t out_bytes = 64 + ((n * 4 + 15) & ~15ull) + ((n + 15) & ~15ull);
+    const size_t out_bytes = kHeaderBytes + ((n * 4 + 15) & ~15ull) + ((n + 15) & ~15ull);
     int rc = e->ws_dec.ensure(in_bytes + out_bytes + 512, in_bytes + out_bytes + 512);
     if (rc) return rc;
     char* h = static_cast<char*>(e->ws_dec.host);
@@ -475,8 +479,8 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     char* dout = d + ((used + 255) & ~size_t(255));
     OutDev od;
     od.header = reinterpret_cast<unsigned long long*>(dout);
-    od.idx = reinterpret_cast<int32_t*>(dout + 64);
-    od.action = reinterpret_cast<uint8_t*>(dout + 64 + ((n * 4 + 15) & ~15ull));
+    od.idx = reinterpret_cast<int32_t*>(dout + kHeaderBytes);
+    od.action = reinterpret_cast<uint8_t*>(dout + kHeaderBytes + ((n * 4 + 15) & ~15ull));
     ReqDev rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
     KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
     const size_t smem = victim_smem(n);
@@ -498,8 +502,8 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
     for (int k = 0; k < 5; ++k) e->stats.k5_phase_ns[k] += static_cast<double>(hdr[4 + k] - hdr[3 + k]);
-    std::memcpy(out_idx, hout + 64, cnt * 4);
-    std::memcpy(out_action, hout + 64 + ((n * 4 + 15) & ~15ull), cnt);
+    std::memcpy(out_idx, hout + kHeaderBytes, cnt * 4);
+    std::memcpy(out_action, hout + kHeaderBytes + ((n * 4 + 15) & ~15ull), cnt);
     *out_count = cnt;
     *out_imm = hdr[1];
     *out_pend = hdr[2];

@@ -1,0 +1,290 @@
+// K5, device-wide path for trees above the single-CTA limit (4096 nodes).
+//
+// Same closed form as the single-CTA kernel (decide.cu), spread over the
+// whole GPU:
+//   1. stage flags (self-eligible, releases-parent) per node            -- 1 grid kernel
+//   2. `before` order of the candidates as a stable LSD radix sort       -- CUB onesweep, one
+//      pass per key word, least significant first: id, seq, time, (rank)  pass per word
+//      and finally a 1-bit "not a candidate" word so non-candidates sort last
+//   3. ord, blocked root walks, R, eff root walks                         -- 4 grid kernels
+//      (global atomics with early exit, as in the CTA version)
+//   4. victims: R sorted by (eff asc, depth desc)                         -- CUB radix sort
+//   5. byte prefix in victim order + the `needed` cut + actions           -- CUB scan + 1 kernel
+// No host round trip between phases; one H2D of the packed SoA and one D2H of the result.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "engine_internal.hpp"
+
+using namespace kvf_impl;
+
+namespace {
+
+constexpr int64_t kSuffix = INT64_MAX / 2;
+constexpr int64_t kUnreach = INT64_MAX / 4;
+
+struct BigTree {
+    const int32_t* parent;
+    const uint16_t* depth;
+    const uint8_t* status;
+    const int32_t* lock;
+    const int64_t* rank;
+    const double* time;
+    const uint64_t* seq;
+    const uint64_t* id;
+    const uint64_t* tokens;
+    const uint8_t* backed;
+    uint32_t n;
+    uint64_t bpt;
+};
+
+struct BigReq {
+    uint64_t needed;
+    int64_t floor;
+    uint64_t cpu_used, cpu_cap;
+    int32_t wa, offload, has_floor;
+};
+
+__device__ __forceinline__ uint64_t time_order(double t) {
+    const uint64_t b = t == 0.0 ? 0ull : static_cast<uint64_t>(__double_as_longlong(t));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void big_stage(BigTree t, BigReq q, uint8_t* flags, uint32_t* blocked, uint32_t* vals) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
+        const uint64_t bytes = t.tokens[i] * t.bpt;
+        const bool cpu_room = q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap;
+        const bool selfok = i > 0 && t.lock[i] == 0 && t.status[i] == 0 && (!q.has_floor || t.rank[i] > q.floor);
+        const bool releases = !q.offload || t.backed[i] || !cpu_room;
+        flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
+        blocked[i] = 0;
+        vals[i] = i;
+    }
+}
+
+// keys[k] = word `w` of node vals[k]'s `before` key (ascending = earlier)
+__global__ void big_gather_key(BigTree t, const uint8_t* flags, const uint32_t* vals, uint64_t* keys, int w) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
+        const uint32_t i = vals[k];
+        uint64_t key;
+        switch (w) {
+            case 0: key = t.id[i]; break;
+            case 1: key = t.seq[i]; break;
+            case 2: key = time_order(t.time[i]); break;
+            case 3: key = ~(static_cast<uint64_t>(t.rank[i]) ^ 0x8000000000000000ull); break;  // rank desc
+            default: key = (flags[i] & 1) ? 0 : 1;                                             // candidates first
+        }
+        keys[k] = key;
+    }
+}
+
+__global__ void big_ord(uint32_t n, const uint32_t* vals, int32_t* ord) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) ord[vals[k]] = k;
+}
+
+__global__ void big_blocked(BigTree t, const uint8_t* flags, uint32_t* blocked) {
+    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < t.n; m += gridDim.x * blockDim.x) {
+        const uint8_t f = flags[m];
+        if (t.status[m] == 1 || ((f & 1) && (f & 2))) continue;
+        for (int32_t cur = static_cast<int32_t>(m);;) {
+            const int32_t p = t.parent[cur];
+            if (p <= 0) break;
+            if (atomicOr(&blocked[p], 1u)) break;
+            if (t.status[p] == 1) break;
+            cur = p;
+        }
+    }
+}
+
+__global__ void big_r_init(uint32_t n, uint8_t* flags, const uint32_t* blocked, const int32_t* ord, int32_t* eff) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool r = (flags[i] & 1) && !blocked[i];
+        if (r) flags[i] |= 4;
+        eff[i] = r ? ord[i] : -1;
+    }
+}
+
+__global__ void big_eff(BigTree t, const uint8_t* flags, const int32_t* ord, int32_t* eff) {
+    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < t.n; m += gridDim.x * blockDim.x) {
+        if (!(flags[m] & 4)) continue;
+        const int32_t v = ord[m];
+        for (int32_t cur = static_cast<int32_t>(m);;) {
+            const int32_t p = t.parent[cur];
+            if (p <= 0 || !(flags[p] & 4)) break;
+            if (atomicMax(&eff[p], v) >= v) break;
+            cur = p;
+        }
+    }
+}
+
+__global__ void big_victim_keys(BigTree t, const uint8_t* flags, const int32_t* eff, uint64_t* keys, uint32_t* vals) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
+        keys[i] = (flags[i] & 4) ? (static_cast<uint64_t>(static_cast<uint32_t>(eff[i])) << 32) |
+                                       (0xFFFFFFFFu - static_cast<uint32_t>(t.depth[i]))
+                                 : ~0ull;
+        vals[i] = i;
+    }
+}
+
+__global__ void big_bytes(BigTree t, const uint64_t* keys, const uint32_t* vals, uint64_t* bytes) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x)
+        bytes[k] = keys[k] == ~0ull ? 0 : t.tokens[vals[k]] * t.bpt;
+}
+
+// victim k is popped iff the bytes freed before it are < needed (radix_cache.cpp:335)
+__global__ void big_cut(BigTree t, BigReq q, const uint64_t* keys, const uint32_t* vals, const uint64_t* before,
+                        int32_t* out_idx, uint8_t* out_act, unsigned long long* header) {
+    uint64_t imm = 0, pend = 0;
+    uint32_t cnt = 0;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
+        if (keys[k] == ~0ull || before[k] >= q.needed) continue;
+        const uint32_t v = vals[k];
+        const uint64_t bytes = t.tokens[v] * t.bpt;
+        uint8_t act;
+        if (!q.offload) act = KVF_ACT_REMOVE;
+        else if (t.backed[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
+        else if (!(q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap)) act = KVF_ACT_REMOVE;
+        else act = KVF_ACT_OFFLOAD;
+        out_idx[k] = static_cast<int32_t>(v);
+        out_act[k] = act;
+        (act == KVF_ACT_OFFLOAD ? pend : imm) += bytes;
+        cnt = max(cnt, k + 1);
+    }
+    for (int o = 16; o; o >>= 1) {
+        imm += __shfl_xor_sync(0xffffffffu, imm, o);
+        pend += __shfl_xor_sync(0xffffffffu, pend, o);
+        cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (cnt) atomicMax(header, static_cast<unsigned long long>(cnt));
+        if (imm) atomicAdd(header + 1, static_cast<unsigned long long>(imm));
+        if (pend) atomicAdd(header + 2, static_cast<unsigned long long>(pend));
+    }
+}
+
+template <typename T>
+T* take(char*& p, size_t count) {
+    T* r = reinterpret_cast<T*>(p);
+    p += (count * sizeof(T) + 255) & ~size_t(255);
+    return r;
+}
+
+}  // namespace
+
+namespace kvf_impl {
+
+int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
+                        uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend) {
+    const uint32_t n = t->n;
+    cudaStream_t s = e->s_dec;
+    // CUB scratch sizes for n items
+    size_t sort_tmp = 0, scan_tmp = 0;
+    KVF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint64_t*>(nullptr),
+                                             static_cast<uint64_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                             static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 64, s));
+    KVF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, static_cast<uint64_t*>(nullptr),
+                                           static_cast<uint64_t*>(nullptr), static_cast<int>(n), s));
+    const size_t in_bytes = static_cast<size_t>(n) * (8 * 5 + 4 * 2 + 2 + 2) + 16 * 256;
+    const size_t work_bytes = static_cast<size_t>(n) * (1 + 4 + 4 + 4 + 8 * 2 + 4 * 2 + 8 * 2 + 4 + 1) +
+                              sort_tmp + scan_tmp + 64 * 256;
+    const size_t out_host = 256 + static_cast<size_t>(n) * 5 + 512;
+    int rc = e->ws_big.ensure(in_bytes + work_bytes, in_bytes + out_host);
+    if (rc) return rc;
+    // ---- pack + one H2D ----
+    char* h = static_cast<char*>(e->ws_big.host);
+    char* hp = h;
+    std::memcpy(take<int64_t>(hp, n), t->rank, n * 8ull);
+    std::memcpy(take<double>(hp, n), t->time, n * 8ull);
+    std::memcpy(take<uint64_t>(hp, n), t->seq, n * 8ull);
+    std::memcpy(take<uint64_t>(hp, n), t->id, n * 8ull);
+    std::memcpy(take<uint64_t>(hp, n), t->tokens, n * 8ull);
+    std::memcpy(take<int32_t>(hp, n), t->parent, n * 4ull);
+    std::memcpy(take<int32_t>(hp, n), t->lock, n * 4ull);
+    std::memcpy(take<uint16_t>(hp, n), t->depth, n * 2ull);
+    std::memcpy(take<uint8_t>(hp, n), t->status, n);
+    std::memcpy(take<uint8_t>(hp, n), t->backed, n);
+    const size_t used = static_cast<size_t>(hp - h);
+    char* d = static_cast<char*>(e->ws_big.dev);
+    char* dp = d;
+    BigTree bt;
+    bt.rank = take<int64_t>(dp, n);
+    bt.time = take<double>(dp, n);
+    bt.seq = take<uint64_t>(dp, n);
+    bt.id = take<uint64_t>(dp, n);
+    bt.tokens = take<uint64_t>(dp, n);
+    bt.parent = take<int32_t>(dp, n);
+    bt.lock = take<int32_t>(dp, n);
+    bt.depth = take<uint16_t>(dp, n);
+    bt.status = take<uint8_t>(dp, n);
+    bt.backed = take<uint8_t>(dp, n);
+    bt.n = n;
+    bt.bpt = t->bytes_per_token;
+    uint8_t* flags = take<uint8_t>(dp, n);
+    uint32_t* blocked = take<uint32_t>(dp, n);
+    int32_t* ord = take<int32_t>(dp, n);
+    int32_t* eff = take<int32_t>(dp, n);
+    uint64_t* keys_a = take<uint64_t>(dp, n);
+    uint64_t* keys_b = take<uint64_t>(dp, n);
+    uint32_t* vals_a = take<uint32_t>(dp, n);
+    uint32_t* vals_b = take<uint32_t>(dp, n);
+    uint64_t* bytes = take<uint64_t>(dp, n);
+    uint64_t* before = take<uint64_t>(dp, n);
+    int32_t* d_idx = take<int32_t>(dp, n);
+    uint8_t* d_act = take<uint8_t>(dp, n);
+    unsigned long long* d_hdr = take<unsigned long long>(dp, 4);
+    void* sort_scratch = take<uint8_t>(dp, sort_tmp);
+    void* scan_scratch = take<uint8_t>(dp, scan_tmp);
+    BigReq rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
+    const uint32_t threads = 256;
+    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((n + threads - 1) / threads, e->sm_count * 8ull));
+    KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, s));
+    KVF_CUDA(cudaMemsetAsync(d_hdr, 0, 32, s));
+    KVF_CUDA(cudaEventRecord(e->dec_start, s));
+    big_stage<<<grid, threads, 0, s>>>(bt, rq, flags, blocked, vals_a);
+    // stable LSD passes: id, seq, time, [rank desc], candidate bit
+    const int words[] = {0, 1, 2, 3, 4};
+    uint32_t launches = 1;
+    for (int w : words) {
+        if (w == 3 && !q->workflow_aware) continue;
+        big_gather_key<<<grid, threads, 0, s>>>(bt, flags, vals_a, keys_a, w);
+        KVF_CUDA(cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
+                                                 static_cast<int>(n), 0, w == 4 ? 1 : 64, s));
+        std::swap(vals_a, vals_b);
+        launches += 2;
+    }
+    big_ord<<<grid, threads, 0, s>>>(n, vals_a, ord);
+    big_blocked<<<grid, threads, 0, s>>>(bt, flags, blocked);
+    big_r_init<<<grid, threads, 0, s>>>(n, flags, blocked, ord, eff);
+    big_eff<<<grid, threads, 0, s>>>(bt, flags, ord, eff);
+    big_victim_keys<<<grid, threads, 0, s>>>(bt, flags, eff, keys_a, vals_a);
+    KVF_CUDA(cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
+                                             static_cast<int>(n), 0, 64, s));
+    big_bytes<<<grid, threads, 0, s>>>(bt, keys_b, vals_b, bytes);
+    KVF_CUDA(cub::DeviceScan::ExclusiveSum(scan_scratch, scan_tmp, bytes, before, static_cast<int>(n), s));
+    big_cut<<<grid, threads, 0, s>>>(bt, rq, keys_b, vals_b, before, d_idx, d_act, d_hdr);
+    KVF_CUDA(cudaGetLastError());
+    KVF_CUDA(cudaEventRecord(e->dec_stop, s));
+    launches += 9;
+    e->stats.kernel_launches += launches;
+    e->stats.decisions++;
+    // ---- one D2H: header, then the victim prefix ----
+    char* ho = h + ((used + 255) & ~size_t(255));
+    KVF_CUDA(cudaMemcpyAsync(ho, d_hdr, 32, cudaMemcpyDeviceToHost, s));
+    KVF_CUDA(cudaStreamSynchronize(s));
+    const uint64_t* hdr = reinterpret_cast<const uint64_t*>(ho);
+    const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
+    if (cnt) {
+        KVF_CUDA(cudaMemcpyAsync(out_idx, d_idx, cnt * 4ull, cudaMemcpyDeviceToHost, s));
+        KVF_CUDA(cudaMemcpyAsync(out_action, d_act, cnt, cudaMemcpyDeviceToHost, s));
+        KVF_CUDA(cudaStreamSynchronize(s));
+    }
+    *out_count = cnt;
+    *out_imm = hdr[1];
+    *out_pend = hdr[2];
+    return KVF_OK;
+}
+
+}  // namespace kvf_impl

@@ -739,6 +739,7 @@ int kvf_engine_destroy(kvf_engine* e) {
         if (s) cudaStreamDestroy(s);
     e->ws_dev.release();
     e->ws_dec.release();
+    e->ws_big.release();
     if (e->d_checksum) cudaFree(e->d_checksum);
     if (e->dev_pool) cudaFree(e->dev_pool);
     if (e->host_pool) {

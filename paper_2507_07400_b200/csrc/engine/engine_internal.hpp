@@ -98,6 +98,7 @@ struct kvf_engine {
 
     kvf_impl::Workspace ws_dev;  // fill / checksum / read staging (s_dev)
     kvf_impl::Workspace ws_dec;  // decision kernels (s_dec)
+    kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
 
     uint64_t* d_checksum = nullptr;
     kvf_stats stats{};
@@ -106,5 +107,7 @@ struct kvf_engine {
 
 namespace kvf_impl {
 int acquire_event(kvf_engine* e, cudaEvent_t* ev);
+int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
+                        uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend);
 void recycle_event(kvf_engine* e, cudaEvent_t ev);
 }  // namespace kvf_impl

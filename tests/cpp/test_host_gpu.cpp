@@ -110,9 +110,10 @@ TEST("evict: match refreshes recency, peek does not") {
         r.put({2, 22}, 2.0);
         if (use_match) CHECK(r.cache.match_prefix({1, 11}, 4.0).matched_tokens == 2);
         else CHECK(r.cache.peek_prefix({1, 11}).matched_tokens == 2);
+        const uint64_t want = r.id_of(use_match ? TokenSeq{2, 22} : TokenSeq{1, 11});  // before it is removed
         EvictOutcome out = r.cache.evict({1, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 5.0);
         REQUIRE(out.victims.size() == 1);
-        CHECK(out.victims[0].node_id == r.id_of(use_match ? TokenSeq{2, 22} : TokenSeq{1, 11}));
+        CHECK(out.victims[0].node_id == want);
     }
 }
 
@@ -131,11 +132,12 @@ TEST("evict: workflow-aware order (suffix, then larger steps) and the rank floor
         r.cache.set_agent_priorities(steps);  // K4
         EvictRequest req{floor ? Bytes(1 << 20) : 9 * kBpt, EvictionPolicy::WorkflowAware, TierMode::Discard, {}};
         if (floor) req.rank_floor_exclusive = rank_for_step(1);
+        const uint64_t a_id = r.id_of({1, 11, 12}), b_id = r.id_of({2, 21, 22}), c_id = r.id_of({3, 31, 32});
         EvictOutcome out = r.cache.evict(req, r.tier, 4.0);  // K5
         REQUIRE(out.victims.size() == (floor ? 2u : 3u));
-        CHECK(out.victims[0].node_id == r.id_of({3, 31, 32}));
-        CHECK(out.victims[1].node_id == r.id_of({1, 11, 12}));
-        if (!floor) CHECK(out.victims[2].node_id == r.id_of({2, 21, 22}));
+        CHECK(out.victims[0].node_id == c_id);
+        CHECK(out.victims[1].node_id == a_id);
+        if (!floor) CHECK(out.victims[2].node_id == b_id);
         CHECK(out.sufficient == !floor);
         if (floor) CHECK(r.cache.peek_prefix({2, 21, 22}).matched_tokens == 3);
     }
@@ -158,9 +160,10 @@ TEST("evict: leaves before parents, a freed parent follows in the same pass; loc
         InsertResult a = r.put({1, 11}, 1.0);
         r.put({2, 22}, 2.0);
         r.cache.lock_root_path(a.path.back());
+        const uint64_t b_id = r.id_of({2, 22});
         EvictOutcome out = r.cache.evict({1 << 20, EvictionPolicy::Lru, TierMode::Discard, {}}, r.tier, 3.0);
         REQUIRE(out.victims.size() == 1);
-        CHECK(out.victims[0].node_id == r.id_of({2, 22}));
+        CHECK(out.victims[0].node_id == b_id);
         CHECK(!out.sufficient);
         r.cache.unlock_root_path(a.path.back());
     }
