@@ -261,7 +261,13 @@ def run_ours(args, rank, world, local):
                 "prefetch_jobs": res["prefetch_jobs"], "reactive_jobs": res["reactive_jobs"],
                 "offload_jobs": res["offload_jobs"],
                 "lockstep_k1_gbs": round(res["prefetch_bytes"] / (res["prefetch_device_ms"] * 1e-3) / 1e9, 3)
-                if res["prefetch_device_ms"] else None},
+                if res["prefetch_device_ms"] else None,
+                "breakdown_ms": {"arrival_decisions": round(res["decision_us_total"] / 1e3, 2),
+                                 "k4_calls": res["priority_calls"], "k4_total": round(res["priority_us"] / 1e3, 2),
+                                 "k5_calls": res["evict_calls"], "k5_total": round(res["evict_us"] / 1e3, 2),
+                                 "fence_wait": round(res["fence_wait_us"] / 1e3, 2),
+                                 "h2d_device": round((res["prefetch_device_ms"] + res["reactive_device_ms"]), 2),
+                                 "d2h_device": round(res["offload_device_ms"], 2)}},
         "latency": {"decision_us_per_agent_step": round(res["decision_us_total"] / steps_e2e, 2),
                     "decision_us_max": round(res["decision_us_max"], 2),
                     "k4_us_per_call": round(res["priority_us"] / max(1, res["priority_calls"]), 2),

@@ -45,6 +45,7 @@ typedef struct {
     int32_t numa_node;
     int32_t audit;        /* TierManager::audit after every event */
     int32_t verify_loads; /* GPU checksum of every H2D-loaded node vs its host copy */
+    int32_t timing;       /* 0 modeled (lockstep parity), 1 measured (hardware in the loop) */
 } kvfh_sim_config;
 
 typedef struct {
@@ -63,6 +64,9 @@ typedef struct {
     uint64_t kernel_launches;
     uint64_t verified_loads, verify_failures;
     uint64_t audits;
+    /* stalls (RequestTrace::stall_seconds, virtual seconds) over measured requests */
+    double stall_total_s;
+    uint64_t stalled_requests, measured_requests;
 } kvfh_sim_result;
 
 const char* kvfh_last_error(void);

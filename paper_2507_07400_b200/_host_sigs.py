@@ -13,7 +13,7 @@ class SimConfig(C.Structure):
         ("layers", C.c_uint32), ("kv_heads_total", C.c_uint32), ("kv_heads_local", C.c_uint32),
         ("head_offset", C.c_uint32), ("head_dim", C.c_uint32), ("device", C.c_int32), ("host_slots", C.c_uint64),
         ("pcie_mode", C.c_uint32), ("pcie_ctas", C.c_uint32), ("numa_node", C.c_int32), ("audit", C.c_int32),
-        ("verify_loads", C.c_int32),
+        ("verify_loads", C.c_int32), ("timing", C.c_int32),
     ]
 
 
@@ -28,7 +28,8 @@ class SimResult(C.Structure):
         ("reactive_device_ms", C.c_double), ("offload_device_ms", C.c_double), ("fence_wait_us", C.c_double),
         ("priority_calls", C.c_uint64), ("evict_calls", C.c_uint64), ("priority_us", C.c_double),
         ("evict_us", C.c_double), ("kernel_launches", C.c_uint64), ("verified_loads", C.c_uint64),
-        ("verify_failures", C.c_uint64), ("audits", C.c_uint64),
+        ("verify_failures", C.c_uint64), ("audits", C.c_uint64), ("stall_total_s", C.c_double),
+        ("stalled_requests", C.c_uint64), ("measured_requests", C.c_uint64),
     ]
 
 

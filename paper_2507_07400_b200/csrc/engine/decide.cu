@@ -36,16 +36,40 @@ constexpr int kThreads = 1024;
 constexpr int32_t kBlocked = INT32_MAX;
 // K5 result header: [count, immediate, pending, phase stamps x6] -> 9 words, padded
 constexpr size_t kHeaderBytes = 128;
+// decision inputs up to this size are read by the kernel straight from mapped pinned memory
+constexpr size_t kZeroCopyBytes = 64 << 10;
 
-__global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* __restrict__ parent, uint32_t n,
+// parent[] and the ranks are staged in shared memory when they fit (n <= kPrioSmemNodes,
+// 48 KB), so the root walks never touch global -- or, for small trees, PCIe-mapped host --
+// memory.
+constexpr uint32_t kPrioSmemNodes = 4096;
+
+__global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* __restrict__ parent_in, uint32_t n,
                                                                 const int32_t* __restrict__ bidx,
                                                                 const int64_t* __restrict__ cand, uint32_t m,
                                                                 long long* out) {
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = kRankSuffix;
+    extern __shared__ __align__(16) uint8_t psm[];
+    long long* rank = reinterpret_cast<long long*>(psm);
+    const bool staged = n <= kPrioSmemNodes;
+    int32_t* parent = staged ? reinterpret_cast<int32_t*>(rank + n) : nullptr;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if (staged) {
+            parent[i] = parent_in[i];
+            rank[i] = kRankSuffix;
+        } else {
+            out[i] = kRankSuffix;
+        }
+    }
     __syncthreads();
+    long long* r = staged ? rank : out;
+    const int32_t* par = staged ? parent : parent_in;
     for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
         const long long c = cand[b];
-        for (int32_t v = bidx[b]; v > 0; v = parent[v]) atomicMin(out + v, c);
+        for (int32_t v = bidx[b]; v > 0; v = par[v]) atomicMin(r + v, c);
+    }
+    if (staged) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = rank[i];
     }
 }
 
@@ -125,7 +149,10 @@ __device__ __forceinline__ uint64_t time_order(double t) {
 
 // Shared-memory layout for n <= 4096 nodes (PN = pow2 >= n):
 //   pk0 u64[PN] | pk1 u64[PN]   phase-1 primary keys by position (later: final keys | prefix)
-//   parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | sel u16[PN] | status u8[n] | flags u8[n]
+//   parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | bytes u64[n] | sel u16[PN]
+//   | depth u16[n] | status u8[n] | flags u8[n] | backed u8[n]
+// Everything the later phases touch is staged here once, so inputs may live in mapped host
+// memory (small trees) without per-phase PCIe round trips.
 // flags: bit0 selfok, bit1 releases, bit2 R
 __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, const ReqDev q, OutDev o) {
     extern __shared__ __align__(16) uint8_t sm[];
@@ -139,9 +166,12 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     int32_t* ord = parent + n;
     int32_t* eff = ord + n;
     uint32_t* blocked = reinterpret_cast<uint32_t*>(eff + n);
-    uint16_t* sel = reinterpret_cast<uint16_t*>(blocked + n);
-    uint8_t* st = reinterpret_cast<uint8_t*>(sel + PN);
+    uint64_t* nbytes = reinterpret_cast<uint64_t*>(blocked + n);  // offset 16*PN + 16*n: 8-aligned
+    uint16_t* sel = reinterpret_cast<uint16_t*>(nbytes + n);
+    uint16_t* dep = sel + PN;
+    uint8_t* st = reinterpret_cast<uint8_t*>(dep + n);
     uint8_t* flags = st + n;
+    uint8_t* bk = flags + n;
     __shared__ uint32_t s_cnt, s_rcnt, s_slow;
     __shared__ unsigned long long s_imm, s_pend, s_warp[32];
     // per-phase timestamps (globaltimer ns) -> header[3..10], read by kvf_get_stats
@@ -170,6 +200,9 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
         const bool releases = !q.offload || t.backed[i] || !cpu_room;
         parent[i] = t.parent[i];
         st[i] = s;
+        nbytes[i] = bytes;
+        dep[i] = t.depth[i];
+        bk[i] = t.backed[i];
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
         blocked[i] = 0;
         ord[i] = -1;
@@ -279,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
         const bool r_node = (flags[i] & 4) != 0;
         const uint32_t k = claim(&s_rcnt, r_node);
         if (r_node)
-            keys[k] = (static_cast<uint64_t>(eff[i]) << 32) | (static_cast<uint64_t>(0xFFFFu - t.depth[i]) << 16) | i;
+            keys[k] = (static_cast<uint64_t>(eff[i]) << 32) | (static_cast<uint64_t>(0xFFFFu - dep[i]) << 16) | i;
     }
     __syncthreads();
     const uint32_t r = s_rcnt;
@@ -297,7 +330,7 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     const uint32_t per = (r + blockDim.x - 1) / blockDim.x;
     const uint32_t lo_k = threadIdx.x * per, hi_k = min(r, (threadIdx.x + 1) * per);
     uint64_t local = 0;
-    for (uint32_t k = lo_k; k < hi_k; ++k) local += t.tokens[keys[k] & 0xFFFFu] * t.bpt;
+    for (uint32_t k = lo_k; k < hi_k; ++k) local += nbytes[keys[k] & 0xFFFFu];
     uint64_t inc = local;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int off = 1; off < 32; off <<= 1) {
@@ -320,11 +353,11 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     uint64_t my_imm = 0, my_pend = 0;
     for (uint32_t k = lo_k; k < hi_k; ++k) {
         const uint32_t v = static_cast<uint32_t>(keys[k] & 0xFFFFu);
-        const uint64_t bytes = t.tokens[v] * t.bpt;
+        const uint64_t bytes = nbytes[v];
         if (run < q.needed) {
             uint8_t act;
             if (!q.offload) act = KVF_ACT_REMOVE;
-            else if (t.backed[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
+            else if (bk[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
             else if (!(q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap)) act = KVF_ACT_REMOVE;
             else act = KVF_ACT_OFFLOAD;
             o.idx[k] = static_cast<int32_t>(v);
@@ -360,7 +393,8 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
 
 size_t victim_smem(uint32_t n) {
     const size_t PN = pow2_ceil(n > 1 ? n : 2);
-    return PN * 16 + static_cast<size_t>(n) * 16 + PN * 2 + 2 * ((n + 15) & ~15u) + 64;
+    return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 8 + PN * 2 + static_cast<size_t>(n) * 2 +
+           3 * ((n + 15) & ~15u) + 64;
 }
 
 uint32_t victim_threads(uint32_t n) {  // one compare-exchange per thread per sort stage
@@ -397,7 +431,7 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     const auto t0 = std::chrono::steady_clock::now();
     for (uint32_t b = 0; b < m; ++b)
         if (bidx[b] < 0 || static_cast<uint32_t>(bidx[b]) >= n) return set_error(KVF_E_UNKNOWN_BOUNDARY_NODE, "boundary index out of range");
-    const size_t in_bytes = ((n * 4 + 15) & ~15ull) + ((m * 4 + 15) & ~15ull) + m * 8 + 16;
+    const size_t in_bytes = ((n * 4 + 15) & ~15ull) + ((m * 4 + 15) & ~15ull) + ((m * 8 + 15) & ~15ull);
     const size_t out_bytes = n * 8;
     int rc = e->ws_dec.ensure(in_bytes + out_bytes + 1024, in_bytes + out_bytes + 1024);
     if (rc) return rc;
@@ -407,23 +441,27 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     std::memcpy(carve<int32_t>(hp, m), bidx, m * 4);
     std::memcpy(carve<int64_t>(hp, m), cand, m * 8);
     const size_t used = static_cast<size_t>(hp - h);
-    char* d = static_cast<char*>(e->ws_dec.dev);
-    char* dp = d;
+    const size_t out_off = (used + 255) & ~size_t(255);
+    // Small trees: the kernel reads its inputs from, and writes its result to, mapped pinned
+    // memory -- one launch + one sync, no memcpy launches.  Large: classic H2D / D2H.
+    const bool zero_copy = in_bytes <= kZeroCopyBytes;
+    char* base = zero_copy ? static_cast<char*>(e->ws_dec.host_dev) : static_cast<char*>(e->ws_dec.dev);
+    char* dp = base;
     int32_t* d_parent = carve<int32_t>(dp, n);
     int32_t* d_bidx = carve<int32_t>(dp, m);
     int64_t* d_cand = carve<int64_t>(dp, m);
-    long long* d_out = reinterpret_cast<long long*>(d + ((used + 255) & ~size_t(255)));
-    KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
+    long long* d_out = reinterpret_cast<long long*>(base + out_off);
+    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
-    kvf_priority_kernel<<<1, kThreads, 0, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out);
+    const size_t smem = n <= kPrioSmemNodes ? n * 12ull : 0;
+    kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out);
     KVF_CUDA(cudaGetLastError());
     KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;
-    // results land in pinned staging (a pageable destination would force a staged copy)
-    KVF_CUDA(cudaMemcpyAsync(h, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
+    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(h + out_off, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
-    std::memcpy(out_rank, h, n * 8);
+    std::memcpy(out_rank, h + out_off, n * 8);
     return finish_decision(e, t0);
 }
 
@@ -461,7 +499,8 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     std::memcpy(carve<uint8_t>(hp, n), t->status, n);
     std::memcpy(carve<uint8_t>(hp, n), t->backed, n);
     const size_t used = static_cast<size_t>(hp - h);
-    char* d = static_cast<char*>(e->ws_dec.dev);
+    const bool zero_copy = used <= kZeroCopyBytes;  // read in place from mapped pinned memory
+    char* d = zero_copy ? static_cast<char*>(e->ws_dec.host_dev) : static_cast<char*>(e->ws_dec.dev);
     char* dp = d;
     TreeDev td;
     td.rank = carve<int64_t>(dp, n);
@@ -482,7 +521,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     od.idx = reinterpret_cast<int32_t*>(dout + kHeaderBytes);
     od.action = reinterpret_cast<uint8_t*>(dout + kHeaderBytes + ((n * 4 + 15) & ~15ull));
     ReqDev rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
-    KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
+    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
     const size_t smem = victim_smem(n);
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
@@ -497,7 +536,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     e->stats.kernel_launches++;
     e->stats.decisions++;
     char* hout = h + ((used + 255) & ~size_t(255));
-    KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));
+    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);

@@ -145,7 +145,8 @@ int Workspace::ensure(size_t dn, size_t hn) {
         if (host) cudaFreeHost(host);
         host = nullptr;
         size_t sz = std::max(hn, host_bytes * 2);
-        KVF_CUDA(cudaHostAlloc(&host, sz, cudaHostAllocDefault));
+        KVF_CUDA(cudaHostAlloc(&host, sz, cudaHostAllocMapped | cudaHostAllocPortable));
+        KVF_CUDA(cudaHostGetDevicePointer(&host_dev, host, 0));
         host_bytes = sz;
     }
     return KVF_OK;
@@ -154,7 +155,7 @@ int Workspace::ensure(size_t dn, size_t hn) {
 void Workspace::release() {
     if (dev) cudaFree(dev);
     if (host) cudaFreeHost(host);
-    dev = host = nullptr;
+    dev = host = host_dev = nullptr;
     dev_bytes = host_bytes = 0;
 }
 
@@ -484,7 +485,9 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         // traffic such as decision inputs (profiles/r01_probe_inflight.txt).  HBM jobs go wide.
         const bool pcie = src.host || dst.host;
         const uint32_t threads = pcie ? 256 : 512, unroll = pcie ? 4 : 8;
-        p.tile_bytes = threads * unroll * (vec16 ? 16 : 8);
+        // a tile is several unrolled batches so the per-tile lookup is amortised: PCIe tiles
+        // 64 KiB (4 batches of 256 x 4 x 16 B), HBM tiles 64 KiB (one batch of 512 x 8 x 16 B)
+        p.tile_bytes = threads * unroll * (vec16 ? 16 : 8) * (pcie ? 4 : 1);
         uint64_t tiles = 0;
         for (uint32_t i = 0; i < np; ++i) {
             const Piece& pc = pieces[first + i];

@@ -62,6 +62,7 @@ struct Workspace {  // grow-only device + pinned staging buffers
     void* dev = nullptr;
     size_t dev_bytes = 0;
     void* host = nullptr;
+    void* host_dev = nullptr;  // device-side alias of `host` (mapped pinned memory)
     size_t host_bytes = 0;
     int ensure(size_t dev_need, size_t host_need);
     void release();

@@ -168,6 +168,7 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
         s->engine = std::make_unique<Engine>(eo);
         s->sim = std::make_unique<Simulator>(cost, sc, w, c->gpu_cap, c->cpu_cap, c->seed, s->engine.get());
         s->sim->verify_loads = c->verify_loads != 0;
+        if (c->timing == 1) s->sim->tier().set_timing(TransferTiming::Measured);
         // record every transition, tagged with the event index (same stream as ref_trace)
         auto prev = s->sim->tier().transition_observer;
         kvfh_sim* raw = s.get();
@@ -270,6 +271,12 @@ int kvfh_sim_result_get(const kvfh_sim* s, kvfh_sim_result* r) {
         r->verified_loads = s->sim->verified_loads;
         r->verify_failures = s->sim->verify_failures;
         r->audits = s->audits;
+        for (const RequestTrace& t : s->result.traces) {
+            if (!t.measured) continue;
+            r->measured_requests++;
+            r->stall_total_s += t.stall_seconds;
+            if (t.stall_seconds > 1e-12) r->stalled_requests++;
+        }
     });
 }
 
