@@ -131,6 +131,23 @@ int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint
 int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* dev_runs,
                     uint32_t n_dev);
 
+/* K1, layer-pipelined: tiles go plane-outermost, and each finished tile bumps
+ * layer_ready[layer] (caller's device array of `layers` uint32, zeroed by the call); layer l
+ * has landed when layer_ready[l] == *tiles_per_layer.  A consumer can start on layer l while
+ * later layers are still on the wire -- the real mechanism behind the reference's
+ * overlap_fraction gate model (proj/src/scheduler.cpp:252-284, :281). */
+int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
+                           const kvf_run* dev_runs, uint32_t n_dev, uint32_t* layer_ready,
+                           uint32_t* tiles_per_layer);
+/* compute-stream helpers (prefill emulation for measurements): wait for a layer, spin for ns
+ * nanoseconds on `ctas` SMs, and bracket compute work as a job for timing. */
+int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t layer, uint32_t target);
+int kvf_compute_spin(kvf_engine* e, uint64_t ns, uint32_t ctas);
+int kvf_compute_job_begin(kvf_engine* e, uint64_t job_id);
+int kvf_compute_job_end(kvf_engine* e, uint64_t job_id);
+/* device time from first_job's start event to last_job's stop event (any streams) */
+int kvf_job_span_ms(kvf_engine* e, uint64_t first_job, uint64_t last_job, float* ms);
+
 /* fences (TierManager::complete): 1 in *done when the job's bytes have landed */
 int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done);
 int kvf_job_wait(kvf_engine* e, uint64_t job_id);
@@ -197,6 +214,7 @@ typedef struct {
     double decision_kernel_ms; /* K4+K5 kernel time, CUDA events on the decision stream */
     double decision_call_us;   /* K4+K5 host round trip (pack, H2D, kernel, D2H, sync)  */
     double k5_phase_ns[5];     /* K5 in-kernel phases: stage, sort, walks, victim sort, scan+out */
+    double k5_phase_cycles[5]; /* the same phases in SM cycles (clock64)                       */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

@@ -60,7 +60,8 @@ class Stats(C.Structure):
     _fields_ = [("kernel_launches", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("dev_bytes", C.c_uint64), ("h2d_jobs", C.c_uint64), ("d2h_jobs", C.c_uint64),
                 ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
-                ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5)]
+                ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5),
+                ("k5_phase_cycles", C.c_double * 5)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature
@@ -81,6 +82,13 @@ _ENGINE_SIGS = {
     "kvf_d2h_scatter": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32]),
     "kvf_dev_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.c_void_p]),
     "kvf_dev_scatter": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(Run), C.c_uint32]),
+    "kvf_h2d_gather_layered": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32,
+                                         C.c_void_p, C.POINTER(C.c_uint32)]),
+    "kvf_compute_wait_layer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]),
+    "kvf_compute_spin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
+    "kvf_compute_job_begin": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "kvf_compute_job_end": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "kvf_job_span_ms": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_float)]),
     "kvf_job_query": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32)]),
     "kvf_job_wait": (C.c_int, [C.c_void_p, C.c_uint64]),
     "kvf_job_elapsed_ms": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_float)]),

@@ -34,38 +34,57 @@ constexpr int64_t kRankUnreachable = INT64_MAX / 4;
 constexpr uint32_t kMaxNodesSingleCta = 4096;
 constexpr int kThreads = 1024;
 constexpr int32_t kBlocked = INT32_MAX;
-// K5 result header: [count, immediate, pending, phase stamps x6] -> 9 words, padded
+// K5 result header: [count, immediate, pending, 6 globaltimer stamps, 6 clock64 stamps]
 constexpr size_t kHeaderBytes = 128;
 // decision inputs up to this size are read by the kernel straight from mapped pinned memory
 constexpr size_t kZeroCopyBytes = 64 << 10;
 
-// parent[] and the ranks are staged in shared memory when they fit (n <= kPrioSmemNodes,
-// 48 KB), so the root walks never touch global -- or, for small trees, PCIe-mapped host --
-// memory.
+// Copy a packed input blob (16-B multiple) into shared memory with all of a thread's loads
+// in flight before its stores: when the blob sits in mapped pinned host memory this costs
+// one PCIe round trip instead of one per input array and phase.
+__device__ __forceinline__ void stage_blob(uint8_t* dst, const uint8_t* src, uint32_t bytes) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    const uint32_t nv = bytes / 16;
+    for (uint32_t base = threadIdx.x; base < nv; base += blockDim.x * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (base + u * blockDim.x < nv) v[u] = s4[base + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (base + u * blockDim.x < nv) d4[base + u * blockDim.x] = v[u];
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ const T* rebase(const T* p, const uint8_t* from, const uint8_t* to) {
+    return reinterpret_cast<const T*>(to + (reinterpret_cast<const uint8_t*>(p) - from));
+}
+
+// The ranks live in shared memory when they fit (n <= kPrioSmemNodes); small inputs are
+// staged there too (stage_blob), so the root walks never touch PCIe-mapped host memory.
 constexpr uint32_t kPrioSmemNodes = 4096;
 
-__global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* __restrict__ parent_in, uint32_t n,
-                                                                const int32_t* __restrict__ bidx,
-                                                                const int64_t* __restrict__ cand, uint32_t m,
-                                                                long long* out) {
+__global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* parent, uint32_t n, const int32_t* bidx,
+                                                                const int64_t* cand, uint32_t m, long long* out,
+                                                                const uint8_t* blob, uint32_t blob_bytes) {
     extern __shared__ __align__(16) uint8_t psm[];
-    long long* rank = reinterpret_cast<long long*>(psm);
     const bool staged = n <= kPrioSmemNodes;
-    int32_t* parent = staged ? reinterpret_cast<int32_t*>(rank + n) : nullptr;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        if (staged) {
-            parent[i] = parent_in[i];
-            rank[i] = kRankSuffix;
-        } else {
-            out[i] = kRankSuffix;
-        }
+    long long* rank = reinterpret_cast<long long*>(psm);
+    if (blob_bytes) {  // inputs -> shared memory in one round trip
+        uint8_t* sb = psm + (staged ? (n * 8ull + 15) & ~15ull : 0ull);
+        stage_blob(sb, blob, blob_bytes);
+        parent = rebase(parent, blob, sb);
+        bidx = rebase(bidx, blob, sb);
+        cand = rebase(cand, blob, sb);
     }
-    __syncthreads();
     long long* r = staged ? rank : out;
-    const int32_t* par = staged ? parent : parent_in;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = kRankSuffix;
+    __syncthreads();
     for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
         const long long c = cand[b];
-        for (int32_t v = bidx[b]; v > 0; v = par[v]) atomicMin(r + v, c);
+        for (int32_t v = bidx[b]; v > 0; v = parent[v]) atomicMin(r + v, c);
     }
     if (staged) {
         __syncthreads();
@@ -86,6 +105,8 @@ struct TreeDev {
     const uint8_t* backed;
     uint32_t n;
     uint64_t bpt;
+    const uint8_t* blob;  // packed inputs to stage into shared memory first (nullptr: read in place)
+    uint32_t blob_bytes;
 };
 
 struct ReqDev {
@@ -154,8 +175,9 @@ __device__ __forceinline__ uint64_t time_order(double t) {
 // Everything the later phases touch is staged here once, so inputs may live in mapped host
 // memory (small trees) without per-phase PCIe round trips.
 // flags: bit0 selfok, bit1 releases, bit2 R
-__global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, const ReqDev q, OutDev o) {
+__global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in, const ReqDev q, OutDev o) {
     extern __shared__ __align__(16) uint8_t sm[];
+    TreeDev t = t_in;
     const uint32_t n = t.n;
     const uint32_t PN = pow2_ceil(n > 1 ? n : 2);
     uint64_t* pk0 = reinterpret_cast<uint64_t*>(sm);
@@ -180,9 +202,25 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
             unsigned long long t_ns;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns));
             o.header[3 + k] = t_ns;
+            o.header[9 + k] = clock64();  // SM cycles: finer than globaltimer for short phases
         }
     };
     stamp(0);
+    if (t.blob_bytes) {  // small trees: the whole snapshot -> shared memory in one round trip
+        uint8_t* sb = bk + ((n + 15) & ~15u);
+        sb = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sb) + 15) & ~uintptr_t(15));
+        stage_blob(sb, t.blob, t.blob_bytes);
+        t.parent = rebase(t.parent, t.blob, sb);
+        t.depth = rebase(t.depth, t.blob, sb);
+        t.status = rebase(t.status, t.blob, sb);
+        t.lock = rebase(t.lock, t.blob, sb);
+        t.rank = rebase(t.rank, t.blob, sb);
+        t.time = rebase(t.time, t.blob, sb);
+        t.seq = rebase(t.seq, t.blob, sb);
+        t.id = rebase(t.id, t.blob, sb);
+        t.tokens = rebase(t.tokens, t.blob, sb);
+        t.backed = rebase(t.backed, t.blob, sb);
+    }
     if (threadIdx.x == 0) {
         s_cnt = s_rcnt = s_slow = 0;
         s_imm = s_pend = 0;
@@ -240,14 +278,14 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     // 2. candidates in `before` order -> ord
     auto full_after = [&](uint32_t x, uint32_t y) {  // is node x after node y?
         if (wa) {
-            const int64_t rx = __ldg(t.rank + x), ry = __ldg(t.rank + y);
+            const int64_t rx = t.rank[x], ry = t.rank[y];
             if (rx != ry) return rx < ry;
         }
-        const double tx = __ldg(t.time + x), ty = __ldg(t.time + y);
+        const double tx = t.time[x], ty = t.time[y];
         if (tx != ty) return tx > ty;
-        const uint64_t sx = __ldg(t.seq + x), sy = __ldg(t.seq + y);
+        const uint64_t sx = t.seq[x], sy = t.seq[y];
         if (sx != sy) return sx > sy;
-        return __ldg(t.id + x) > __ldg(t.id + y);
+        return t.id[x] > t.id[y];
     };
     bitonic(
         P,
@@ -391,10 +429,10 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t, c
     stamp(5);
 }
 
-size_t victim_smem(uint32_t n) {
+size_t victim_smem(uint32_t n, size_t blob = 0) {
     const size_t PN = pow2_ceil(n > 1 ? n : 2);
     return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 8 + PN * 2 + static_cast<size_t>(n) * 2 +
-           3 * ((n + 15) & ~15u) + 64;
+           3 * ((n + 15) & ~15u) + 64 + (blob ? blob + 32 : 0);
 }
 
 uint32_t victim_threads(uint32_t n) {  // one compare-exchange per thread per sort stage
@@ -453,8 +491,15 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     long long* d_out = reinterpret_cast<long long*>(base + out_off);
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
-    const size_t smem = n <= kPrioSmemNodes ? n * 12ull : 0;
-    kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out);
+    const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_copy ? used : 0);
+    if (smem > 48 * 1024 && !e->prio_attr_set) {
+        KVF_CUDA(cudaFuncSetAttribute(kvf_priority_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kPrioSmemNodes * 8 + kZeroCopyBytes + 64)));
+        e->prio_attr_set = true;
+    }
+    kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
+                                                         zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
+                                                         zero_copy ? static_cast<uint32_t>(used) : 0u);
     KVF_CUDA(cudaGetLastError());
     KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
@@ -515,6 +560,8 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     td.backed = carve<uint8_t>(dp, n);
     td.n = n;
     td.bpt = t->bytes_per_token;
+    td.blob = zero_copy ? reinterpret_cast<const uint8_t*>(d) : nullptr;
+    td.blob_bytes = zero_copy ? static_cast<uint32_t>(used) : 0u;
     char* dout = d + ((used + 255) & ~size_t(255));
     OutDev od;
     od.header = reinterpret_cast<unsigned long long*>(dout);
@@ -522,12 +569,11 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     od.action = reinterpret_cast<uint8_t*>(dout + kHeaderBytes + ((n * 4 + 15) & ~15ull));
     ReqDev rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
-    const size_t smem = victim_smem(n);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    const size_t smem = victim_smem(n, zero_copy ? used : 0);
+    if (smem > 48 * 1024 && !e->victim_attr_set) {  // per engine: attributes are per device
         KVF_CUDA(cudaFuncSetAttribute(kvf_victim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(victim_smem(kMaxNodesSingleCta))));
-        attr = victim_smem(kMaxNodesSingleCta);
+        e->victim_attr_set = true;
     }
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od);
@@ -540,7 +586,10 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
-    for (int k = 0; k < 5; ++k) e->stats.k5_phase_ns[k] += static_cast<double>(hdr[4 + k] - hdr[3 + k]);
+    for (int k = 0; k < 5; ++k) {
+        e->stats.k5_phase_ns[k] += static_cast<double>(hdr[4 + k] - hdr[3 + k]);
+        e->stats.k5_phase_cycles[k] += static_cast<double>(hdr[10 + k] - hdr[9 + k]);
+    }
     std::memcpy(out_idx, hout + kHeaderBytes, cnt * 4);
     std::memcpy(out_action, hout + kHeaderBytes + ((n * 4 + 15) & ~15ull), cnt);
     *out_count = cnt;

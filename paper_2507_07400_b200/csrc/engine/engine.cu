@@ -193,11 +193,14 @@ struct CopyParams {
     uint32_t planes;
     uint32_t npieces;
     uint32_t tile_bytes;
-    uint32_t pad;
+    uint32_t layer_major;  // tiles ordered plane-outermost (layer-pipelined K1)
+    uint64_t plane_tiles;  // layer_major: tiles of one plane (sum over pieces)
+    uint32_t* layer_ready; // layer_major: per-layer finished-tile counters (nullable)
     uint64_t src_off[kMaxPieces];
     uint64_t dst_off[kMaxPieces];
     uint64_t seg[kMaxPieces];             // bytes of the piece in one plane
     uint64_t tile_begin[kMaxPieces + 1];  // prefix over pieces of planes*ceil(seg/tile)
+                                          // (layer_major: of ceil(seg/tile), one plane)
 };
 
 struct TileRef {
@@ -206,7 +209,13 @@ struct TileRef {
     uint32_t len;
 };
 
-__device__ __forceinline__ TileRef locate(const CopyParams& p, uint64_t t) {
+__device__ __forceinline__ TileRef locate(const CopyParams& p, uint64_t t, uint32_t* plane_out = nullptr) {
+    // piece-major: t -> (piece, plane, tile);  layer-major: t -> (plane, piece, tile)
+    uint64_t plane = 0;
+    if (p.layer_major) {
+        plane = t / p.plane_tiles;
+        t -= plane * p.plane_tiles;
+    }
     uint32_t lo = 0, hi = p.npieces - 1;
     while (lo < hi) {
         uint32_t mid = (lo + hi + 1) >> 1;
@@ -215,8 +224,9 @@ __device__ __forceinline__ TileRef locate(const CopyParams& p, uint64_t t) {
     const uint64_t local = t - p.tile_begin[lo];
     const uint64_t seg = p.seg[lo];
     const uint64_t tps = (seg + p.tile_bytes - 1) / p.tile_bytes;
-    const uint64_t plane = local / tps;
-    const uint64_t off = (local - plane * tps) * p.tile_bytes;
+    if (!p.layer_major) plane = local / tps;
+    const uint64_t off = (local - (p.layer_major ? 0 : plane * tps)) * p.tile_bytes;
+    if (plane_out) *plane_out = static_cast<uint32_t>(plane);
     TileRef r;
     r.s = p.src + plane * p.src_stride + p.src_off[lo] + off;
     r.d = p.dst + plane * p.dst_stride + p.dst_off[lo] + off;
@@ -250,7 +260,8 @@ __device__ __forceinline__ void st_stream(uint2* ptr, const uint2& v) {
 template <typename V, int UNROLL>
 __global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant__ CopyParams p) {
     for (uint64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        const TileRef r = locate(p, t);
+        uint32_t plane = 0;
+        const TileRef r = locate(p, t, &plane);
         const V* s = reinterpret_cast<const V*>(r.s);
         V* d = reinterpret_cast<V*>(r.d);
         const uint32_t nvec = r.len / sizeof(V);
@@ -267,7 +278,30 @@ __global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant
                 if (i < nvec) st_stream(d + i, v[u]);
             }
         }
+        if (p.layer_ready) {  // publish: this tile of layer plane/2 has landed
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(p.layer_ready + plane / 2, 1u);
+        }
     }
+}
+
+// Consumer side of the layer-pipelined load: hold the compute stream until layer `l` has
+// all its tiles (cf. the reference's overlap_fraction gate, proj/src/scheduler.cpp:281).
+__global__ void kvf_wait_layer_kernel(const uint32_t* ready, uint32_t l, uint32_t target) {
+    if (threadIdx.x != 0) return;
+    while (atomicAdd(const_cast<uint32_t*>(ready) + l, 0u) < target) __nanosleep(256);
+    __threadfence();
+}
+
+// Prefill emulation for measurements: occupy `ctas` SMs for `ns` nanoseconds.
+__global__ void kvf_spin_kernel(uint64_t ns) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(100);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
 }
 
 // ---- K1/K2 bulk path: the TMA bulk-copy engine moves CHUNK-byte pieces global->smem
@@ -458,7 +492,9 @@ struct Endpoint {
 
 // Launch the copy of `pieces` (all planes) between two pools on `stream`.
 int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const Endpoint& dst,
-                const std::vector<Piece>& pieces, uint32_t mode, uint32_t ctas) {
+                const std::vector<Piece>& pieces, uint32_t mode, uint32_t ctas, uint32_t* layer_ready = nullptr,
+                uint64_t* tiles_per_layer = nullptr) {
+    if (layer_ready) mode = KVF_COPY_SM_VEC;  // only the vector kernel publishes per-layer progress
     const uint64_t tpb = e->tpb;
     for (size_t first = 0; first < pieces.size(); first += kMaxPieces) {
         const uint32_t np = static_cast<uint32_t>(std::min<size_t>(kMaxPieces, pieces.size() - first));
@@ -489,25 +525,32 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         // 64 KiB (4 batches of 256 x 4 x 16 B), HBM tiles 64 KiB (one batch of 512 x 8 x 16 B)
         p.tile_bytes = threads * unroll * (vec16 ? 16 : 8) * (pcie ? 4 : 1);
         uint64_t tiles = 0;
+        const uint64_t per_piece_planes = layer_ready ? 1 : e->planes;
         for (uint32_t i = 0; i < np; ++i) {
             const Piece& pc = pieces[first + i];
             p.src_off[i] = pc.src_slot * tpb;
             p.dst_off[i] = pc.dst_slot * tpb;
             p.seg[i] = pc.ntok * tpb;
             p.tile_begin[i] = tiles;
-            tiles += static_cast<uint64_t>(e->planes) * ((p.seg[i] + p.tile_bytes - 1) / p.tile_bytes);
+            tiles += per_piece_planes * ((p.seg[i] + p.tile_bytes - 1) / p.tile_bytes);
         }
         p.tile_begin[np] = tiles;
+        if (layer_ready) {  // plane-outermost order + per-layer counters
+            p.layer_major = 1;
+            p.plane_tiles = tiles;
+            p.layer_ready = layer_ready;
+            if (tiles_per_layer) *tiles_per_layer += 2 * tiles;
+            tiles *= e->planes;
+        }
         p.total_tiles = tiles;
         if (tiles == 0) continue;
         uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(ctas, tiles));
         if (mode == KVF_COPY_SM_BULK && vec16) {
             const size_t smem = static_cast<size_t>(kBulkStages) * kBulkChunk;
-            static bool attr_set = false;
-            if (!attr_set) {
+            if (!e->bulk_attr_set) {  // per engine: attributes are per device
                 KVF_CUDA(cudaFuncSetAttribute(kvf_copy_bulk_kernel<kBulkStages, kBulkChunk>,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                attr_set = true;
+                e->bulk_attr_set = true;
             }
             kvf_copy_bulk_kernel<kBulkStages, kBulkChunk><<<grid, 32, smem, stream>>>(p);
         } else if (vec16) {
@@ -823,6 +866,76 @@ int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uin
                     uint32_t n_host) {
     KVF_GUARD(e);
     return transfer(e, job_id, KVF_TIER_DEVICE, dev_runs, n_dev, KVF_TIER_HOST, host_runs, n_host);
+}
+
+int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
+                           const kvf_run* dev_runs, uint32_t n_dev, uint32_t* layer_ready, uint32_t* tiles_per_layer) {
+    KVF_GUARD(e);
+    if (!layer_ready || !tiles_per_layer) return set_error(KVF_E_INVALID_ARG, "null layer_ready / tiles_per_layer");
+    uint64_t ts = 0, td = 0;
+    if (!runs_valid(e, KVF_TIER_HOST, host_runs, n_host, &ts) || !runs_valid(e, KVF_TIER_DEVICE, dev_runs, n_dev, &td))
+        return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    if (ts != td) return set_error(KVF_E_INVALID_ARG, "source and destination token counts differ");
+    std::vector<Piece> pieces;
+    merge_runs(host_runs, n_host, dev_runs, n_dev, pieces);
+    Job j;
+    int rc = begin_job(e, job_id, e->s_h2d, j);
+    if (rc) return rc;
+    if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_h2d, e->dev_write_done, 0));
+    KVF_CUDA(cudaMemsetAsync(layer_ready, 0, e->geom.layers * sizeof(uint32_t), e->s_h2d));
+    Endpoint src{e->host_pool_dev, e->host_slots * e->tpb, true};
+    Endpoint dst{e->dev_pool, e->dev_slots * e->tpb, false};
+    uint64_t per_layer = 0;
+    rc = launch_copy(e, e->s_h2d, src, dst, pieces, KVF_COPY_SM_VEC, e->cfg.pcie_ctas, layer_ready, &per_layer);
+    if (rc) return rc;
+    *tiles_per_layer = static_cast<uint32_t>(per_layer);
+    j.bytes = ts * e->token_bytes;
+    e->stats.h2d_bytes += j.bytes;
+    e->stats.h2d_jobs++;
+    return end_job(e, job_id, j);
+}
+
+int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t layer, uint32_t target) {
+    KVF_GUARD(e);
+    if (!layer_ready || layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "bad layer");
+    kvf_wait_layer_kernel<<<1, 32, 0, e->s_dev>>>(layer_ready, layer, target);
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    return KVF_OK;
+}
+
+int kvf_compute_spin(kvf_engine* e, uint64_t ns, uint32_t ctas) {
+    KVF_GUARD(e);
+    kvf_spin_kernel<<<ctas ? ctas : 1, 32, 0, e->s_dev>>>(ns);
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    return KVF_OK;
+}
+
+int kvf_compute_job_begin(kvf_engine* e, uint64_t job_id) {
+    KVF_GUARD(e);
+    Job j;
+    int rc = begin_job(e, job_id, e->s_dev, j);
+    if (rc) return rc;
+    e->jobs.emplace(job_id, j);  // stop event recorded by kvf_compute_job_end
+    return KVF_OK;
+}
+
+int kvf_compute_job_end(kvf_engine* e, uint64_t job_id) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    KVF_CUDA(cudaEventRecord(it->second.stop, it->second.stream));
+    return KVF_OK;
+}
+
+int kvf_job_span_ms(kvf_engine* e, uint64_t first_job, uint64_t last_job, float* ms) {
+    KVF_GUARD(e);
+    auto a = e->jobs.find(first_job), b = e->jobs.find(last_job);
+    if (a == e->jobs.end() || b == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job");
+    KVF_CUDA(cudaEventSynchronize(b->second.stop));
+    KVF_CUDA(cudaEventElapsedTime(ms, a->second.start, b->second.stop));
+    return KVF_OK;
 }
 
 int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* runs, uint32_t n, void* staging) {

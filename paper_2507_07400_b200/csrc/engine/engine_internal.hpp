@@ -102,6 +102,7 @@ struct kvf_engine {
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
 
     uint64_t* d_checksum = nullptr;
+    bool victim_attr_set = false, prio_attr_set = false, bulk_attr_set = false;
     kvf_stats stats{};
     std::mutex mu;  // engine calls are serialised per engine
 };

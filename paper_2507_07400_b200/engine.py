@@ -100,6 +100,34 @@ class Engine:
                                           N.runs_array(host_runs), len(host_runs)))
         return job
 
+    def h2d_layered(self, host_runs, dev_runs, layer_ready_ptr, job=None):
+        """Layer-pipelined K1; returns (job, tiles_per_layer)."""
+        job = job or self.new_job()
+        tpl = C.c_uint32()
+        N.check(self._lib.kvf_h2d_gather_layered(self.h, job, N.runs_array(host_runs), len(host_runs),
+                                                 N.runs_array(dev_runs), len(dev_runs), layer_ready_ptr,
+                                                 C.byref(tpl)))
+        return job, tpl.value
+
+    def compute_wait_layer(self, layer_ready_ptr, layer, target):
+        N.check(self._lib.kvf_compute_wait_layer(self.h, layer_ready_ptr, layer, target))
+
+    def compute_spin(self, ns, ctas=1):
+        N.check(self._lib.kvf_compute_spin(self.h, int(ns), ctas))
+
+    def compute_begin(self, job=None):
+        job = job or self.new_job()
+        N.check(self._lib.kvf_compute_job_begin(self.h, job))
+        return job
+
+    def compute_end(self, job):
+        N.check(self._lib.kvf_compute_job_end(self.h, job))
+
+    def span_ms(self, first_job, last_job):
+        ms = C.c_float()
+        N.check(self._lib.kvf_job_span_ms(self.h, first_job, last_job, C.byref(ms)))
+        return ms.value
+
     def dev_gather(self, dev_runs, staging_ptr, job=None):
         job = job or self.new_job()
         N.check(self._lib.kvf_dev_gather(self.h, job, N.runs_array(dev_runs), len(dev_runs), staging_ptr))
@@ -158,7 +186,7 @@ class Engine:
     def stats(self):
         s = N.Stats()
         N.check(self._lib.kvf_get_stats(self.h, C.byref(s)))
-        return {f: (list(getattr(s, f)) if f == "k5_phase_ns" else getattr(s, f)) for f, _ in N.Stats._fields_}
+        return {f: (list(getattr(s, f)) if f.startswith("k5_phase") else getattr(s, f)) for f, _ in N.Stats._fields_}
 
     # ---- decisions ---------------------------------------------------------------------
     def priority(self, parent, bidx, cand):

@@ -57,6 +57,8 @@ def main():
             row[f"k5_call_us_{key}"] = round((s1["decision_call_us"] - s0["decision_call_us"]) / reps, 2)
             row[f"k5_python_us_{key}"] = round(wall, 2)
             row[f"k5_phase_us_{key}"] = [round((b - a) / reps / 1e3, 2) for a, b in zip(s0["k5_phase_ns"], s1["k5_phase_ns"])]
+            row[f"k5_phase_kcycles_{key}"] = [round((b - a) / reps / 1e3, 2)
+                                              for a, b in zip(s0["k5_phase_cycles"], s1["k5_phase_cycles"])]
         w0 = time.perf_counter()
         for _ in range(reps):
             oracle_evict(c)

@@ -1,0 +1,50 @@
+"""Layer-pipelined K1 (kvf_h2d_gather_layered): same bytes as K1, tiles landed
+layer by layer, and a compute-stream consumer can start on layer l before later layers land."""
+import numpy as np
+import pytest
+
+from oracle_ffi import Geom, lib as olib, runs_array as oruns
+
+pytestmark = pytest.mark.gpu
+N = pytest.importorskip("paper_2507_07400_b200._native")
+torch = pytest.importorskip("torch")
+from paper_2507_07400_b200.engine import Engine  # noqa: E402
+
+
+def test_layered_load_bytes_and_counters():
+    L = 8
+    with Engine(layers=L, kv_heads_total=8, head_dim=128, gpu_slots=4096, host_slots=4096) as e:
+        rng = np.random.default_rng(3)
+        ntok = 1500
+        cids = rng.integers(0, 2**63, size=ntok, dtype=np.uint64)
+        h = e.alloc(N.KVF_TIER_HOST, 700) + e.alloc(N.KVF_TIER_HOST, 800)
+        e.fill(N.KVF_TIER_HOST, h, cids)
+        d = e.alloc(N.KVF_TIER_DEVICE, 300) + e.alloc(N.KVF_TIER_DEVICE, 1200)
+        ready = torch.zeros(L, dtype=torch.int32, device="cuda")
+        j, tpl = e.h2d_layered(h, d, ready.data_ptr())
+        e.wait(j)
+        e.release(j)
+        torch.cuda.synchronize()
+        assert tpl > 0 and ready.cpu().tolist() == [tpl] * L
+        want = np.zeros(ntok * e.token_bytes, dtype=np.uint8)
+        olib().kvfo_fill(Geom(L, 8, 128, 0), want.ctypes.data, ntok, oruns([(0, ntok)]), 1, cids.ctypes.data)
+        assert np.array_equal(e.read(N.KVF_TIER_DEVICE, d), want)
+
+
+def test_consumer_starts_before_the_load_finishes():
+    L = 32
+    with Engine(layers=L, kv_heads_total=8, head_dim=128, gpu_slots=8192, host_slots=8192) as e:
+        h = e.alloc(N.KVF_TIER_HOST, 8192)
+        d = e.alloc(N.KVF_TIER_DEVICE, 8192)
+        ready = torch.zeros(L, dtype=torch.int32, device="cuda")
+        j, tpl = e.h2d_layered(h, d, ready.data_ptr())
+        c0 = e.compute_begin()
+        e.compute_wait_layer(ready.data_ptr(), 0, tpl)
+        c1 = e.compute_begin()  # layer 0 ready
+        e.compute_end(c1)
+        e.compute_end(c0)
+        first = e.span_ms(j, c1)   # load start -> layer 0 usable
+        total = e.elapsed_ms(j)    # load start -> all layers landed
+        assert first < total / 4, (first, total)
+        for x in (j, c0, c1):
+            e.release(x)
