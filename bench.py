@@ -130,9 +130,15 @@ def run_ours(args, rank, world, local):
     from paper_2507_07400_b200.engine import Engine
     from paper_2507_07400_b200.sim import Sim
 
+    # KVF_BENCH_SAME_DEVICE=1 maps every rank to GPU 0 and uses gloo: a 1-GPU rehearsal of the
+    # N-rank code path (tests/test_bench_contract.py); real runs use one GPU per rank + NCCL.
+    same_dev = os.environ.get("KVF_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if same_dev or not torch.cuda.is_available() else "nccl"
     if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
     from paper_2507_07400_b200.shard import plan
     sp = plan(rank, world, layers=32, kv_heads=8, head_dim=128, gpu_budget=BUDGET_FULL)
     heads, bpt, budget = sp.kv_heads_local, sp.bytes_per_token, sp.gpu_budget
@@ -209,7 +215,7 @@ def run_ours(args, rank, world, local):
     }
     if world > 1:
         t = torch.tensor([total_step_ms, wall, e2e_wall, mine["k1_avg_ms"], float(not ok)], dtype=torch.float64,
-                         device=f"cuda:{local}")
+                         device="cpu" if backend == "gloo" else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_step_ms, wall, e2e_wall, k1_avg, notok = t.tolist()
         ok = not notok

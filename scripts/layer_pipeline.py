@@ -32,10 +32,11 @@ def main():
     for mode in ("serial", "pipelined"):
         best = None
         for _ in range(4):
-            if mode == "serial":
-                j = e.h2d(h, d)
-                e.wait(j)
+            if mode == "serial":  # a fence on the whole node, then the prefill (device-side wait)
+                j, tpl = e.h2d_layered(h, d, ready.data_ptr())
                 c = e.compute_begin()
+                for l in range(L):
+                    e.compute_wait_layer(ready.data_ptr(), l, tpl)
                 for _l in range(L):
                     e.compute_spin(per_layer_ns)
                 e.compute_end(c)

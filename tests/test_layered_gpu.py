@@ -37,14 +37,15 @@ def test_consumer_starts_before_the_load_finishes():
         h = e.alloc(N.KVF_TIER_HOST, 8192)
         d = e.alloc(N.KVF_TIER_DEVICE, 8192)
         ready = torch.zeros(L, dtype=torch.int32, device="cuda")
-        j, tpl = e.h2d_layered(h, d, ready.data_ptr())
-        c0 = e.compute_begin()
-        e.compute_wait_layer(ready.data_ptr(), 0, tpl)
-        c1 = e.compute_begin()  # layer 0 ready
-        e.compute_end(c1)
-        e.compute_end(c0)
-        first = e.span_ms(j, c1)   # load start -> layer 0 usable
-        total = e.elapsed_ms(j)    # load start -> all layers landed
+        for rep in range(2):  # rep 0 also loads the kernels (lazy module loading)
+            j, tpl = e.h2d_layered(h, d, ready.data_ptr())
+            c0 = e.compute_begin()
+            e.compute_wait_layer(ready.data_ptr(), 0, tpl)
+            c1 = e.compute_begin()  # layer 0 ready
+            e.compute_end(c1)
+            e.compute_end(c0)
+            first = e.span_ms(j, c1)   # load start -> layer 0 usable
+            total = e.elapsed_ms(j)    # load start -> all layers landed
+            for x in (j, c0, c1):
+                e.release(x)
         assert first < total / 4, (first, total)
-        for x in (j, c0, c1):
-            e.release(x)
