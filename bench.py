@@ -257,6 +257,9 @@ def run_ours(args, rank, world, local):
                          "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(k3_gbs / peaks["hbm_gbs"], 4),
                          "peak_source": peak_src},
         "pcie_peaks_gbs": {k: round(v, 3) for k, v in pcie.items()},
+        # the reference's own figure for this transfer is its cost model: 64e9 * 0.6 B/s + 50 us
+        # per job (proj/src/cost_model.cpp:47-50) -> 38.33 GB/s for a 1 GiB node
+        "vs_reference_cost_model": round(value / world / ((1 << 30) / ((1 << 30) / (64e9 * 0.6) + 50e-6) / 1e9), 3),
         "cpu_baseline": cpu,
         "e2e": {"value": round(res["prefetch_bytes"] * world / e2e_wall / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(h2d_all * world / steps_e2e),

@@ -162,6 +162,45 @@ __device__ __forceinline__ void bitonic(uint32_t P, Greater greater, Swap swap) 
     __syncthreads();
 }
 
+// Register bitonic sort of P <= 64 elements by warp 0: lane l holds positions l and l + 32.
+// Stages with j < 32 exchange with __shfl_xor_sync, the j = 32 stage is in-register; no
+// shared-memory traffic and no barriers (the common case: BASELINE trees have <= 64
+// candidates).  `after(a, b)`: a sorts after b.
+template <typename T>
+__device__ __forceinline__ T shfl_xor_t(const T& v, int m);
+template <>
+__device__ __forceinline__ uint64_t shfl_xor_t(const uint64_t& v, int m) {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+}
+struct CandKey {
+    uint64_t k0, k1;
+    uint32_t idx;
+};
+template <>
+__device__ __forceinline__ CandKey shfl_xor_t(const CandKey& v, int m) {
+    return CandKey{__shfl_xor_sync(0xffffffffu, v.k0, m), __shfl_xor_sync(0xffffffffu, v.k1, m),
+                   __shfl_xor_sync(0xffffffffu, v.idx, m)};
+}
+
+template <typename T, typename After>
+__device__ __forceinline__ void warp_bitonic64(T (&v)[2], uint32_t P, After after) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = 2; k <= P; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            T nv[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t pos = lane + 32 * e;
+                const T other = j >= 32 ? v[e ^ 1] : shfl_xor_t(v[e], static_cast<int>(j));
+                const bool lower = (pos & j) == 0, asc = (pos & k) == 0;
+                // the lower slot keeps the smaller element when ascending
+                nv[e] = (lower == asc) ? (after(v[e], other) ? other : v[e]) : (after(other, v[e]) ? other : v[e]);
+            }
+            v[0] = nv[0];
+            v[1] = nv[1];
+        }
+}
+
 // Order-preserving u64 image of a double (-0.0 == +0.0 as in the reference's `!=`).
 __device__ __forceinline__ uint64_t time_order(double t) {
     const uint64_t b = t == 0.0 ? 0ull : static_cast<uint64_t>(__double_as_longlong(t));
@@ -287,7 +326,30 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
         if (sx != sy) return sx > sy;
         return t.id[x] > t.id[y];
     };
-    bitonic(
+    if (P <= 64) {  // small trees: warp 0 sorts in registers
+        if (threadIdx.x < 32) {
+            CandKey v[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t pos = threadIdx.x + 32 * e;
+                v[e] = pos < P ? CandKey{pk0[pos], pk1[pos], sel[pos]} : CandKey{~0ull, ~0ull, 0xFFFFu};
+            }
+            warp_bitonic64(v, P, [&](const CandKey& a, const CandKey& b) {
+                if (a.idx == 0xFFFFu || b.idx == 0xFFFFu) return a.idx == 0xFFFFu && b.idx != 0xFFFFu;
+                if (!slow) {
+                    if (a.k0 != b.k0) return a.k0 > b.k0;
+                    if (a.k1 != b.k1) return a.k1 > b.k1;
+                }
+                return full_after(a.idx, b.idx);
+            });
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t pos = threadIdx.x + 32 * e;
+                if (pos < P) sel[pos] = static_cast<uint16_t>(v[e].idx);
+            }
+        }
+        __syncthreads();
+    } else bitonic(
         P,
         [&](uint32_t a, uint32_t b) {  // element at a must come after element at b
             const uint32_t x = sel[a], y = sel[b];
@@ -356,13 +418,32 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
     const uint32_t r = s_rcnt;
     const uint32_t PR = pow2_ceil(r > 1 ? r : 2);
     for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
-    bitonic(
-        PR, [&](uint32_t a, uint32_t b) { return keys[a] > keys[b]; },
-        [&](uint32_t a, uint32_t b) {
-            const uint64_t x = keys[a];
-            keys[a] = keys[b];
-            keys[b] = x;
-        });
+    if (PR <= 64) {
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint64_t v[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t pos = threadIdx.x + 32 * e;
+                v[e] = pos < PR ? keys[pos] : ~0ull;
+            }
+            warp_bitonic64(v, PR, [](uint64_t a, uint64_t b) { return a > b; });
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t pos = threadIdx.x + 32 * e;
+                if (pos < PR) keys[pos] = v[e];
+            }
+        }
+        __syncthreads();
+    } else {
+        bitonic(
+            PR, [&](uint32_t a, uint32_t b) { return keys[a] > keys[b]; },
+            [&](uint32_t a, uint32_t b) {
+                const uint64_t x = keys[a];
+                keys[a] = keys[b];
+                keys[b] = x;
+            });
+    }
     stamp(4);
     // 6. exclusive byte prefix in victim order (block scan)
     const uint32_t per = (r + blockDim.x - 1) / blockDim.x;

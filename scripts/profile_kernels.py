@@ -42,16 +42,18 @@ def main(which):
             e.wait(j)
             print(which, f"{e.elapsed_ms(j):.3f} ms")
             e.release(j)
-    if which == "k5":
+    if which in ("k5", "k5small"):
         from oracle_ffi import TreeArrays, load_jsonl
-        cases = sorted(load_jsonl("evict_medium.jsonl"), key=lambda c: -len(c["parent"]))
-        c = cases[0]
+        if which == "k5":
+            c = sorted(load_jsonl("evict_medium.jsonl"), key=lambda c: -len(c["parent"]))[0]
+        else:  # a BASELINE-sized tree (~44 nodes, like C1/C2)
+            c = min(load_jsonl("evict_small.jsonl"), key=lambda c: abs(len(c["parent"]) - 44))
         ta = TreeArrays(c)
         tree = {k: getattr(ta, k) for k in ("parent", "status", "lock", "rank", "time", "seq", "id", "tokens",
                                             "backed")}
         tree["depth"] = depth_from_parent(ta.parent)
         tree["bpt"] = ta.bpt
-        for _ in range(3):
+        for _ in range(6):
             e.victims(tree, c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"], c["cpu_used"],
                       c["cpu_cap"])
         print("k5 nodes", ta.n)
