@@ -135,9 +135,13 @@ __device__ __forceinline__ uint32_t claim(uint32_t* counter, bool take) {
 }
 
 __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
+#else
     uint32_t p = 1;
     while (p < x) p <<= 1;
     return p;
+#endif
 }
 
 // Bitonic sort over P (power of two) elements with one compare-exchange per pair index.
@@ -162,43 +166,22 @@ __device__ __forceinline__ void bitonic(uint32_t P, Greater greater, Swap swap) 
     __syncthreads();
 }
 
-// Register bitonic sort of P <= 64 elements by warp 0: lane l holds positions l and l + 32.
-// Stages with j < 32 exchange with __shfl_xor_sync, the j = 32 stage is in-register; no
-// shared-memory traffic and no barriers (the common case: BASELINE trees have <= 64
-// candidates).  `after(a, b)`: a sorts after b.
-template <typename T>
-__device__ __forceinline__ T shfl_xor_t(const T& v, int m);
-template <>
-__device__ __forceinline__ uint64_t shfl_xor_t(const uint64_t& v, int m) {
-    return __shfl_xor_sync(0xffffffffu, v, m);
-}
-struct CandKey {
-    uint64_t k0, k1;
-    uint32_t idx;
-};
-template <>
-__device__ __forceinline__ CandKey shfl_xor_t(const CandKey& v, int m) {
-    return CandKey{__shfl_xor_sync(0xffffffffu, v.k0, m), __shfl_xor_sync(0xffffffffu, v.k1, m),
-                   __shfl_xor_sync(0xffffffffu, v.idx, m)};
-}
-
-template <typename T, typename After>
-__device__ __forceinline__ void warp_bitonic64(T (&v)[2], uint32_t P, After after) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            T nv[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint32_t pos = lane + 32 * e;
-                const T other = j >= 32 ? v[e ^ 1] : shfl_xor_t(v[e], static_cast<int>(j));
-                const bool lower = (pos & j) == 0, asc = (pos & k) == 0;
-                // the lower slot keeps the smaller element when ascending
-                nv[e] = (lower == asc) ? (after(v[e], other) ? other : v[e]) : (after(other, v[e]) ? other : v[e]);
-            }
-            v[0] = nv[0];
-            v[1] = nv[1];
-        }
+// Rank sort for <= 64 elements: element i's output position is the number of elements that
+// sort before it.  G = blockDim.x / 64 consecutive lanes share element i and split the j range,
+// so each thread runs c / G independent comparisons (ILP instead of the 21 dependent stages a
+// 64-wide bitonic network needs) and a G-lane shuffle reduction finishes the count.
+template <typename Before>
+__device__ __forceinline__ uint32_t rank64(uint32_t c, Before before, uint32_t& i_out) {
+    const uint32_t G = blockDim.x >> 6;  // >= 2: small trees launch >= 128 threads
+    const uint32_t i = threadIdx.x / G, q = threadIdx.x % G;
+    uint32_t cnt = 0;
+    if (i < c) {
+#pragma unroll 4
+        for (uint32_t j = q; j < c; j += G) cnt += (j != i && before(j, i)) ? 1u : 0u;
+    }
+    for (uint32_t off = G >> 1; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    i_out = (q == 0 && i < c) ? i : 0xFFFFFFFFu;
+    return cnt;
 }
 
 // Order-preserving u64 image of a double (-0.0 == +0.0 as in the reference's `!=`).
@@ -326,30 +309,23 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
         if (sx != sy) return sx > sy;
         return t.id[x] > t.id[y];
     };
-    if (P <= 64) {  // small trees: warp 0 sorts in registers
-        if (threadIdx.x < 32) {
-            CandKey v[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint32_t pos = threadIdx.x + 32 * e;
-                v[e] = pos < P ? CandKey{pk0[pos], pk1[pos], sel[pos]} : CandKey{~0ull, ~0ull, 0xFFFFu};
-            }
-            warp_bitonic64(v, P, [&](const CandKey& a, const CandKey& b) {
-                if (a.idx == 0xFFFFu || b.idx == 0xFFFFu) return a.idx == 0xFFFFu && b.idx != 0xFFFFu;
-                if (!slow) {
-                    if (a.k0 != b.k0) return a.k0 > b.k0;
-                    if (a.k1 != b.k1) return a.k1 > b.k1;
-                }
-                return full_after(a.idx, b.idx);
-            });
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint32_t pos = threadIdx.x + 32 * e;
-                if (pos < P) sel[pos] = static_cast<uint16_t>(v[e].idx);
-            }
-        }
+    if (P <= 64) {  // small trees: rank sort straight into ord
         __syncthreads();
-    } else bitonic(
+        uint32_t i;
+        const uint32_t rk = rank64(
+            c,
+            [&](uint32_t a, uint32_t b) {  // candidate a sorts before candidate b
+                if (!slow) {
+                    if (pk0[a] != pk0[b]) return pk0[a] < pk0[b];
+                    if (pk1[a] != pk1[b]) return pk1[a] < pk1[b];
+                }
+                return full_after(sel[b], sel[a]);
+            },
+            i);
+        if (i != 0xFFFFFFFFu) ord[sel[i]] = static_cast<int32_t>(rk);
+        __syncthreads();
+    } else {
+        bitonic(
         P,
         [&](uint32_t a, uint32_t b) {  // element at a must come after element at b
             const uint32_t x = sel[a], y = sel[b];
@@ -370,7 +346,8 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
             pk0[b] = p0;
             pk1[b] = p1;
         });
-    for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) ord[sel[k]] = static_cast<int32_t>(k);
+        for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) ord[sel[k]] = static_cast<int32_t>(k);
+    }
     stamp(2);
     // 3. blocked(n): some node of n's device subtree (below n) is not self-eligible or would
     //    not release it (has_device_child, radix_cache.cpp:40-45).  Every such node walks up
@@ -418,23 +395,15 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
     const uint32_t r = s_rcnt;
     const uint32_t PR = pow2_ceil(r > 1 ? r : 2);
     for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
-    if (PR <= 64) {
+    if (PR <= 64) {  // keys are unique: rank sort into the spare pk1 half, then swap roles
         __syncthreads();
-        if (threadIdx.x < 32) {
-            uint64_t v[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint32_t pos = threadIdx.x + 32 * e;
-                v[e] = pos < PR ? keys[pos] : ~0ull;
-            }
-            warp_bitonic64(v, PR, [](uint64_t a, uint64_t b) { return a > b; });
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const uint32_t pos = threadIdx.x + 32 * e;
-                if (pos < PR) keys[pos] = v[e];
-            }
-        }
+        uint32_t i;
+        const uint32_t rk = rank64(r, [&](uint32_t a, uint32_t b) { return keys[a] < keys[b]; }, i);
+        if (i != 0xFFFFFFFFu) pref[rk] = keys[i];
         __syncthreads();
+        uint64_t* tmp = keys;
+        keys = pref;
+        pref = tmp;
     } else {
         bitonic(
             PR, [&](uint32_t a, uint32_t b) { return keys[a] > keys[b]; },
@@ -518,7 +487,7 @@ size_t victim_smem(uint32_t n, size_t blob = 0) {
 
 uint32_t victim_threads(uint32_t n) {  // one compare-exchange per thread per sort stage
     const uint32_t half = pow2_ceil(n > 1 ? n : 2) / 2;
-    return half < 32 ? 32 : (half > static_cast<uint32_t>(kThreads) ? kThreads : half);
+    return half < 128 ? 128 : (half > static_cast<uint32_t>(kThreads) ? kThreads : half);
 }
 
 int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
