@@ -139,9 +139,12 @@ int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const k
 int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
                            const kvf_run* dev_runs, uint32_t n_dev, uint32_t* layer_ready,
                            uint32_t* tiles_per_layer);
-/* compute-stream helpers (prefill emulation for measurements): wait for a layer, spin for ns
- * nanoseconds on `ctas` SMs, and bracket compute work as a job for timing. */
+/* compute-stream helpers (model compute emulation for measurements and the wall-clock
+ * driver, on the engine's own compute stream): wait for a layer of a layered load, wait for a
+ * whole transfer job (its stop event), spin for ns nanoseconds on `ctas` SMs, and bracket
+ * compute work as a job (kvf_job_query / kvf_job_elapsed_ms / kvf_job_release apply). */
 int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t layer, uint32_t target);
+int kvf_compute_wait_job(kvf_engine* e, uint64_t job_id);
 int kvf_compute_spin(kvf_engine* e, uint64_t ns, uint32_t ctas);
 int kvf_compute_job_begin(kvf_engine* e, uint64_t job_id);
 int kvf_compute_job_end(kvf_engine* e, uint64_t job_id);

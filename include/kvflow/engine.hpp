@@ -57,6 +57,12 @@ public:
     void release(uint64_t job);
     void sync();
 
+    // emulated model compute on the engine's compute stream (wall-clock driver)
+    void compute_begin(uint64_t job);
+    void compute_end(uint64_t job);
+    void compute_wait_job(uint64_t transfer_job);
+    void compute_spin(uint64_t ns, uint32_t ctas);
+
     void fill(int tier, const RunList& runs, const std::vector<uint64_t>& cids);
     uint64_t checksum(int tier, const RunList& runs);
     uint64_t payload_checksum(const std::vector<uint64_t>& cids);

@@ -46,6 +46,13 @@ typedef struct {
     int32_t audit;        /* TierManager::audit after every event */
     int32_t verify_loads; /* GPU checksum of every H2D-loaded node vs its host copy */
     int32_t timing;       /* 0 modeled (lockstep parity), 1 measured (hardware in the loop) */
+    /* clock: 0 virtual (event-driven on modeled/measured times), 1 wall clock -- transfers and
+     * model compute (spin kernels on the engine's compute stream, cost-model durations scaled
+     * by compute_scale) complete when their CUDA events fire; stalls are real seconds. */
+    int32_t clock;
+    double compute_scale;   /* wall clock: emulated compute = cost-model time * scale (0 -> 1) */
+    uint32_t compute_ctas;  /* wall clock: CTAs the compute emulation spins on (0 -> 128) */
+    int32_t prefetch_retry; /* re-run the step-1 prefetch whenever a transfer lands */
 } kvfh_sim_config;
 
 typedef struct {

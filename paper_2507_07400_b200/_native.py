@@ -85,6 +85,7 @@ _ENGINE_SIGS = {
     "kvf_h2d_gather_layered": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32,
                                          C.c_void_p, C.POINTER(C.c_uint32)]),
     "kvf_compute_wait_layer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]),
+    "kvf_compute_wait_job": (C.c_int, [C.c_void_p, C.c_uint64]),
     "kvf_compute_spin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
     "kvf_compute_job_begin": (C.c_int, [C.c_void_p, C.c_uint64]),
     "kvf_compute_job_end": (C.c_int, [C.c_void_p, C.c_uint64]),

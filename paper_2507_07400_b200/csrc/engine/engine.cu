@@ -755,6 +755,7 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
     if ((err = cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
         (err = cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking)) != cudaSuccess ||
         (err = cudaStreamCreateWithFlags(&e->s_dev, cudaStreamNonBlocking)) != cudaSuccess ||
+        (err = cudaStreamCreateWithFlags(&e->s_cmp, cudaStreamNonBlocking)) != cudaSuccess ||
         (err = cudaStreamCreateWithPriority(&e->s_dec, cudaStreamNonBlocking, hi)) != cudaSuccess)
         return fail(cuda_error(err, "cudaStreamCreate"));
     if ((err = cudaEventCreateWithFlags(&e->dev_write_done, cudaEventDisableTiming)) != cudaSuccess ||
@@ -781,7 +782,7 @@ int kvf_engine_destroy(kvf_engine* e) {
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
     for (cudaEvent_t ev : {e->dev_write_done, e->dec_start, e->dec_stop})
         if (ev) cudaEventDestroy(ev);
-    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec})
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp})
         if (s) cudaStreamDestroy(s);
     e->ws_dev.release();
     e->ws_dec.release();
@@ -898,7 +899,7 @@ int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_r
 int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t layer, uint32_t target) {
     KVF_GUARD(e);
     if (!layer_ready || layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "bad layer");
-    kvf_wait_layer_kernel<<<1, 32, 0, e->s_dev>>>(layer_ready, layer, target);
+    kvf_wait_layer_kernel<<<1, 32, 0, e->s_cmp>>>(layer_ready, layer, target);
     KVF_CUDA(cudaGetLastError());
     e->stats.kernel_launches++;
     return KVF_OK;
@@ -906,16 +907,24 @@ int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t 
 
 int kvf_compute_spin(kvf_engine* e, uint64_t ns, uint32_t ctas) {
     KVF_GUARD(e);
-    kvf_spin_kernel<<<ctas ? ctas : 1, 32, 0, e->s_dev>>>(ns);
+    kvf_spin_kernel<<<ctas ? ctas : 1, 32, 0, e->s_cmp>>>(ns);
     KVF_CUDA(cudaGetLastError());
     e->stats.kernel_launches++;
+    return KVF_OK;
+}
+
+int kvf_compute_wait_job(kvf_engine* e, uint64_t job_id) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    KVF_CUDA(cudaStreamWaitEvent(e->s_cmp, it->second.stop, 0));
     return KVF_OK;
 }
 
 int kvf_compute_job_begin(kvf_engine* e, uint64_t job_id) {
     KVF_GUARD(e);
     Job j;
-    int rc = begin_job(e, job_id, e->s_dev, j);
+    int rc = begin_job(e, job_id, e->s_cmp, j);
     if (rc) return rc;
     e->jobs.emplace(job_id, j);  // stop event recorded by kvf_compute_job_end
     return KVF_OK;
@@ -992,7 +1001,7 @@ int kvf_job_release(kvf_engine* e, uint64_t job_id) {
 
 int kvf_sync_all(kvf_engine* e) {
     KVF_GUARD(e);
-    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec}) KVF_CUDA(cudaStreamSynchronize(s));
+    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp}) KVF_CUDA(cudaStreamSynchronize(s));
     return KVF_OK;
 }
 

@@ -90,6 +90,7 @@ struct kvf_engine {
     kvf_impl::SlotAllocator alloc[2];
 
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_dev = nullptr, s_dec = nullptr;
+    cudaStream_t s_cmp = nullptr;  // emulated model compute (kvf_compute_*): never behind a fill
     cudaEvent_t dev_write_done = nullptr;  // last fill / K3 scatter on s_dev
     cudaEvent_t dec_start = nullptr, dec_stop = nullptr;  // decision kernel timing
     bool dev_write_pending = false;

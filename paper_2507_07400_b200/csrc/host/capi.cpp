@@ -115,6 +115,8 @@ void kvfh_default_config(kvfh_sim_config* c) {
     c->kv_heads_local = 8;
     c->head_dim = 128;
     c->numa_node = -1;
+    c->compute_scale = 1.0;
+    c->compute_ctas = 128;
 }
 
 int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
@@ -169,6 +171,12 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
         s->sim = std::make_unique<Simulator>(cost, sc, w, c->gpu_cap, c->cpu_cap, c->seed, s->engine.get());
         s->sim->verify_loads = c->verify_loads != 0;
         if (c->timing == 1) s->sim->tier().set_timing(TransferTiming::Measured);
+        if (c->clock == 1) {
+            s->sim->clock = ClockMode::WallClock;
+            s->sim->wall.compute_scale = c->compute_scale > 0 ? c->compute_scale : 1.0;
+            s->sim->wall.compute_ctas = c->compute_ctas ? c->compute_ctas : 128;
+        }
+        s->sim->wall.prefetch_retry = c->prefetch_retry != 0;
         // record every transition, tagged with the event index (same stream as ref_trace)
         auto prev = s->sim->tier().transition_observer;
         kvfh_sim* raw = s.get();

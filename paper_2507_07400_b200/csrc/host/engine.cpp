@@ -99,6 +99,10 @@ float Engine::elapsed_ms(uint64_t job) {
 }
 
 void Engine::release(uint64_t job) { KVF_CALL(kvf_job_release(e_, job)); }
+void Engine::compute_begin(uint64_t job) { KVF_CALL(kvf_compute_job_begin(e_, job)); }
+void Engine::compute_end(uint64_t job) { KVF_CALL(kvf_compute_job_end(e_, job)); }
+void Engine::compute_wait_job(uint64_t job) { KVF_CALL(kvf_compute_wait_job(e_, job)); }
+void Engine::compute_spin(uint64_t ns, uint32_t ctas) { KVF_CALL(kvf_compute_spin(e_, ns, ctas)); }
 void Engine::sync() { KVF_CALL(kvf_sync_all(e_)); }
 
 void Engine::fill(int tier, const RunList& runs, const std::vector<uint64_t>& cids) {

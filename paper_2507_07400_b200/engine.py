@@ -112,6 +112,9 @@ class Engine:
     def compute_wait_layer(self, layer_ready_ptr, layer, target):
         N.check(self._lib.kvf_compute_wait_layer(self.h, layer_ready_ptr, layer, target))
 
+    def compute_wait_job(self, job):
+        N.check(self._lib.kvf_compute_wait_job(self.h, job))
+
     def compute_spin(self, ns, ctas=1):
         N.check(self._lib.kvf_compute_spin(self.h, int(ns), ctas))
 

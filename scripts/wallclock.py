@@ -1,0 +1,53 @@
+"""Real-time workflow runs on one B200 (ClockMode::WallClock): KVFLOW vs the reference's
+baselines on BASELINE configs C1/C2, compute emulated at cost-model speed, PCIe real.
+Prints one JSON object: per policy and config, makespan, stall totals and per-step latency."""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2507_07400_b200 import sim as S  # noqa: E402
+
+CONFIGS = {"C1": dict(fixed=2048, gpu_cap=855638016), "C2": dict(fixed=8192, gpu_cap=3271557120)}
+
+
+def one(policy, cfg, **kw):
+    with S.Sim(clock=1, policy=policy, **cfg, **kw) as s:
+        s.run()
+        res = s.result()
+        tr = s.trace()
+    m = [r for r in tr if r["t"] == "req" and r["measured"]]
+    lat = [r["done"] - r["arrival"] for r in m]
+    return {
+        "makespan_s": round(res["makespan"], 4),
+        "stall_total_s": round(res["stall_total_s"], 4),
+        "stalled_requests": res["stalled_requests"],
+        "measured_requests": res["measured_requests"],
+        "step_latency_mean_s": round(statistics.mean(lat), 4),
+        "step_latency_p50_s": round(statistics.median(lat), 4),
+        "prefetch_jobs": res["prefetch_jobs"], "reactive_jobs": res["reactive_jobs"],
+        "offload_jobs": res["offload_jobs"],
+        "loaded_GB": round(res["loaded_bytes"] / 1e9, 3),
+        "h2d_GBps": round(res["prefetch_bytes"] + res["reactive_bytes"]) / 1e6 /
+        max(1e-9, res["prefetch_device_ms"] + res["reactive_device_ms"]),
+        "decision_us_mean": round(res["decision_us_total"] / max(1, res["arrivals"]), 1),
+    }
+
+
+def main():
+    out = {}
+    for name, cfg in CONFIGS.items():
+        for pol in ("LRU_GPU_ONLY", "LRU_REACTIVE_HICACHE", "KVFLOW"):
+            out[f"{name}/{pol}"] = one(pol, cfg)
+        out[f"{name}/KVFLOW+retry"] = one("KVFLOW", cfg, prefetch_retry=1)
+    for name in CONFIGS:
+        k = out[f"{name}/KVFLOW"]["step_latency_mean_s"]
+        out[f"{name}/speedup_vs_hicache"] = round(out[f"{name}/LRU_REACTIVE_HICACHE"]["step_latency_mean_s"] / k, 3)
+        out[f"{name}/speedup_vs_gpu_only"] = round(out[f"{name}/LRU_GPU_ONLY"]["step_latency_mean_s"] / k, 3)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
