@@ -139,6 +139,10 @@ int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const k
 int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
                            const kvf_run* dev_runs, uint32_t n_dev, uint32_t* layer_ready,
                            uint32_t* tiles_per_layer);
+/* layer_ready == NULL: the engine owns the counters (64 concurrent layered jobs); the compute
+ * stream then waits for layer `layer` of the job with kvf_compute_wait_job_layer.  Jobs that
+ * are not layered degrade to a whole-job wait.  tiles_per_layer may be NULL in this mode. */
+int kvf_compute_wait_job_layer(kvf_engine* e, uint64_t job_id, uint32_t layer);
 /* compute-stream helpers (model compute emulation for measurements and the wall-clock
  * driver, on the engine's own compute stream): wait for a layer of a layered load, wait for a
  * whole transfer job (its stop event), spin for ns nanoseconds on `ctas` SMs, and bracket

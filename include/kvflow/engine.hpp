@@ -50,6 +50,8 @@ public:
     uint64_t free_tokens(int tier) const;
 
     void h2d(uint64_t job, const RunList& host, const RunList& dev);
+    // layer-pipelined K1 with engine-owned per-layer landed counters
+    void h2d_layered(uint64_t job, const RunList& host, const RunList& dev);
     void d2h(uint64_t job, const RunList& dev, const RunList& host);
     bool query(uint64_t job);
     void wait(uint64_t job);
@@ -61,6 +63,7 @@ public:
     void compute_begin(uint64_t job);
     void compute_end(uint64_t job);
     void compute_wait_job(uint64_t transfer_job);
+    void compute_wait_job_layer(uint64_t transfer_job, uint32_t layer);
     void compute_spin(uint64_t ns, uint32_t ctas);
 
     void fill(int tier, const RunList& runs, const std::vector<uint64_t>& cids);

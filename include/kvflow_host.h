@@ -53,6 +53,7 @@ typedef struct {
     double compute_scale;   /* wall clock: emulated compute = cost-model time * scale (0 -> 1) */
     uint32_t compute_ctas;  /* wall clock: CTAs the compute emulation spins on (0 -> 128) */
     int32_t prefetch_retry; /* re-run the step-1 prefetch whenever a transfer lands */
+    int32_t layered_gate;   /* wall clock: HiCache-gated prefills consume layer-pipelined loads */
 } kvfh_sim_config;
 
 typedef struct {

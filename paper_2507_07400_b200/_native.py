@@ -19,7 +19,7 @@ HOST_SO = os.path.join(PKG, "libkvflow_host.so")
 KVF_OK = 0
 KVF_TIER_DEVICE, KVF_TIER_HOST = 0, 1
 KVF_COPY_SM_VEC, KVF_COPY_SM_BULK, KVF_COPY_CE = 0, 1, 2
-KVF_E_NO_DEVICE = 103
+KVF_E_INVALID_ARG, KVF_E_OUT_OF_HOST_SLOTS, KVF_E_NO_DEVICE, KVF_E_UNKNOWN_JOB, KVF_E_TOO_LARGE = 101, 102, 103, 104, 105
 
 
 class KvfError(RuntimeError):
@@ -86,6 +86,7 @@ _ENGINE_SIGS = {
                                          C.c_void_p, C.POINTER(C.c_uint32)]),
     "kvf_compute_wait_layer": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]),
     "kvf_compute_wait_job": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "kvf_compute_wait_job_layer": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
     "kvf_compute_spin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32]),
     "kvf_compute_job_begin": (C.c_int, [C.c_void_p, C.c_uint64]),
     "kvf_compute_job_end": (C.c_int, [C.c_void_p, C.c_uint64]),

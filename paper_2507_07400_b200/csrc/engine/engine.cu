@@ -763,6 +763,12 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
         return fail(cuda_error(err, "cudaEventCreate"));
     if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_checksum), sizeof(uint64_t))) != cudaSuccess)
         return fail(cuda_error(err, "cudaMalloc(checksum)"));
+    const size_t ctr_bytes = static_cast<size_t>(kvf_impl::kLayerSlots) * e->geom.layers * sizeof(uint32_t);
+    if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_layer_ctr), ctr_bytes)) != cudaSuccess ||
+        (err = cudaMemset(e->d_layer_ctr, 0, ctr_bytes)) != cudaSuccess)
+        return fail(cuda_error(err, "cudaMalloc(layer counters)"));
+    e->lr_total.assign(kvf_impl::kLayerSlots, 0);
+    for (int32_t k = static_cast<int32_t>(kvf_impl::kLayerSlots) - 1; k >= 0; --k) e->lr_free.push_back(k);
     // Size the staging workspaces once: growing them later means cudaFree (a device-wide
     // sync) and cudaHostAlloc inside a decision call -- milliseconds on the hot path.
     if (int rc = e->ws_dec.ensure(1u << 20, 1u << 20)) return fail(rc);
@@ -788,6 +794,7 @@ int kvf_engine_destroy(kvf_engine* e) {
     e->ws_dec.release();
     e->ws_big.release();
     if (e->d_checksum) cudaFree(e->d_checksum);
+    if (e->d_layer_ctr) cudaFree(e->d_layer_ctr);
     if (e->dev_pool) cudaFree(e->dev_pool);
     if (e->host_pool) {
         if (e->host_registered) {
@@ -872,7 +879,8 @@ int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uin
 int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,
                            const kvf_run* dev_runs, uint32_t n_dev, uint32_t* layer_ready, uint32_t* tiles_per_layer) {
     KVF_GUARD(e);
-    if (!layer_ready || !tiles_per_layer) return set_error(KVF_E_INVALID_ARG, "null layer_ready / tiles_per_layer");
+    const bool owned = layer_ready == nullptr;  // engine-owned counters (kvf_compute_wait_job_layer)
+    if (owned && e->lr_free.empty()) return set_error(KVF_E_TOO_LARGE, "all layered-load counter slots in flight");
     uint64_t ts = 0, td = 0;
     if (!runs_valid(e, KVF_TIER_HOST, host_runs, n_host, &ts) || !runs_valid(e, KVF_TIER_DEVICE, dev_runs, n_dev, &td))
         return set_error(KVF_E_INVALID_ARG, "run out of pool range");
@@ -883,13 +891,27 @@ int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_r
     int rc = begin_job(e, job_id, e->s_h2d, j);
     if (rc) return rc;
     if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_h2d, e->dev_write_done, 0));
-    KVF_CUDA(cudaMemsetAsync(layer_ready, 0, e->geom.layers * sizeof(uint32_t), e->s_h2d));
+    if (owned) {  // counters only grow: no reset, so a late waiter on a recycled slot never hangs
+        j.lr_slot = e->lr_free.back();
+        e->lr_free.pop_back();
+        layer_ready = e->d_layer_ctr + static_cast<size_t>(j.lr_slot) * e->geom.layers;
+    } else {
+        KVF_CUDA(cudaMemsetAsync(layer_ready, 0, e->geom.layers * sizeof(uint32_t), e->s_h2d));
+    }
     Endpoint src{e->host_pool_dev, e->host_slots * e->tpb, true};
     Endpoint dst{e->dev_pool, e->dev_slots * e->tpb, false};
     uint64_t per_layer = 0;
     rc = launch_copy(e, e->s_h2d, src, dst, pieces, KVF_COPY_SM_VEC, e->cfg.pcie_ctas, layer_ready, &per_layer);
-    if (rc) return rc;
-    *tiles_per_layer = static_cast<uint32_t>(per_layer);
+    if (rc) {
+        if (owned) e->lr_free.push_back(j.lr_slot);
+        return rc;
+    }
+    if (tiles_per_layer) *tiles_per_layer = static_cast<uint32_t>(per_layer);
+    if (owned) {
+        j.lr_base = e->lr_total[j.lr_slot];
+        j.lr_tpl = static_cast<uint32_t>(per_layer);
+        e->lr_total[j.lr_slot] += j.lr_tpl;
+    }
     j.bytes = ts * e->token_bytes;
     e->stats.h2d_bytes += j.bytes;
     e->stats.h2d_jobs++;
@@ -908,6 +930,23 @@ int kvf_compute_wait_layer(kvf_engine* e, const uint32_t* layer_ready, uint32_t 
 int kvf_compute_spin(kvf_engine* e, uint64_t ns, uint32_t ctas) {
     KVF_GUARD(e);
     kvf_spin_kernel<<<ctas ? ctas : 1, 32, 0, e->s_cmp>>>(ns);
+    KVF_CUDA(cudaGetLastError());
+    e->stats.kernel_launches++;
+    return KVF_OK;
+}
+
+int kvf_compute_wait_job_layer(kvf_engine* e, uint64_t job_id, uint32_t layer) {
+    KVF_GUARD(e);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    if (layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "bad layer");
+    const kvf_impl::Job& j = it->second;
+    if (j.lr_slot < 0) {  // not a layered job: the whole transfer is the dependency
+        KVF_CUDA(cudaStreamWaitEvent(e->s_cmp, j.stop, 0));
+        return KVF_OK;
+    }
+    kvf_wait_layer_kernel<<<1, 32, 0, e->s_cmp>>>(e->d_layer_ctr + static_cast<size_t>(j.lr_slot) * e->geom.layers,
+                                                 layer, j.lr_base + j.lr_tpl);
     KVF_CUDA(cudaGetLastError());
     e->stats.kernel_launches++;
     return KVF_OK;
@@ -995,6 +1034,7 @@ int kvf_job_release(kvf_engine* e, uint64_t job_id) {
     KVF_CUDA(cudaEventSynchronize(it->second.stop));
     recycle_event(e, it->second.start);
     recycle_event(e, it->second.stop);
+    if (it->second.lr_slot >= 0) e->lr_free.push_back(it->second.lr_slot);
     e->jobs.erase(it);
     return KVF_OK;
 }

@@ -56,7 +56,13 @@ struct Job {
     cudaEvent_t start = nullptr, stop = nullptr;
     cudaStream_t stream = nullptr;
     uint64_t bytes = 0;
+    // layered H2D with engine-owned counters: slot, and layer l has landed once
+    // counters[slot][l] >= lr_base + lr_tpl (counters only grow; never reset)
+    int32_t lr_slot = -1;
+    uint32_t lr_base = 0, lr_tpl = 0;
 };
+
+constexpr uint32_t kLayerSlots = 64;  // concurrent layered loads with engine-owned counters
 
 struct Workspace {  // grow-only device + pinned staging buffers
     void* dev = nullptr;
@@ -103,6 +109,9 @@ struct kvf_engine {
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
 
     uint64_t* d_checksum = nullptr;
+    uint32_t* d_layer_ctr = nullptr;       // [kLayerSlots][layers] landed-tile counters
+    std::vector<uint32_t> lr_total;         // host mirror: tiles ever published per layer, per slot
+    std::vector<int32_t> lr_free;           // free counter slots
     bool victim_attr_set = false, prio_attr_set = false, bulk_attr_set = false;
     kvf_stats stats{};
     std::mutex mu;  // engine calls are serialised per engine

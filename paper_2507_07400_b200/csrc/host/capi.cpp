@@ -177,6 +177,7 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
             s->sim->wall.compute_ctas = c->compute_ctas ? c->compute_ctas : 128;
         }
         s->sim->wall.prefetch_retry = c->prefetch_retry != 0;
+        s->sim->wall.layered_gate = c->layered_gate != 0;
         // record every transition, tagged with the event index (same stream as ref_trace)
         auto prev = s->sim->tier().transition_observer;
         kvfh_sim* raw = s.get();

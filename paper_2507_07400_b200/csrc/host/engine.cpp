@@ -79,6 +79,11 @@ void Engine::h2d(uint64_t job, const RunList& host, const RunList& dev) {
                             static_cast<uint32_t>(dev.size())));
 }
 
+void Engine::h2d_layered(uint64_t job, const RunList& host, const RunList& dev) {
+    KVF_CALL(kvf_h2d_gather_layered(e_, job, host.data(), static_cast<uint32_t>(host.size()), dev.data(),
+                                    static_cast<uint32_t>(dev.size()), nullptr, nullptr));
+}
+
 void Engine::d2h(uint64_t job, const RunList& dev, const RunList& host) {
     KVF_CALL(kvf_d2h_scatter(e_, job, dev.data(), static_cast<uint32_t>(dev.size()), host.data(),
                              static_cast<uint32_t>(host.size())));
@@ -102,6 +107,9 @@ void Engine::release(uint64_t job) { KVF_CALL(kvf_job_release(e_, job)); }
 void Engine::compute_begin(uint64_t job) { KVF_CALL(kvf_compute_job_begin(e_, job)); }
 void Engine::compute_end(uint64_t job) { KVF_CALL(kvf_compute_job_end(e_, job)); }
 void Engine::compute_wait_job(uint64_t job) { KVF_CALL(kvf_compute_wait_job(e_, job)); }
+void Engine::compute_wait_job_layer(uint64_t job, uint32_t layer) {
+    KVF_CALL(kvf_compute_wait_job_layer(e_, job, layer));
+}
 void Engine::compute_spin(uint64_t ns, uint32_t ctas) { KVF_CALL(kvf_compute_spin(e_, ns, ctas)); }
 void Engine::sync() { KVF_CALL(kvf_sync_all(e_)); }
 

@@ -115,6 +115,9 @@ class Engine:
     def compute_wait_job(self, job):
         N.check(self._lib.kvf_compute_wait_job(self.h, job))
 
+    def compute_wait_job_layer(self, job, layer):
+        N.check(self._lib.kvf_compute_wait_job_layer(self.h, job, layer))
+
     def compute_spin(self, ns, ctas=1):
         N.check(self._lib.kvf_compute_spin(self.h, int(ns), ctas))
 

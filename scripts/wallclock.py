@@ -42,6 +42,7 @@ def main():
         for pol in ("LRU_GPU_ONLY", "LRU_REACTIVE_HICACHE", "KVFLOW"):
             out[f"{name}/{pol}"] = one(pol, cfg)
         out[f"{name}/KVFLOW+retry"] = one("KVFLOW", cfg, prefetch_retry=1)
+        out[f"{name}/LRU_REACTIVE_HICACHE+layered"] = one("LRU_REACTIVE_HICACHE", cfg, layered_gate=1)
     for name in CONFIGS:
         k = out[f"{name}/KVFLOW"]["step_latency_mean_s"]
         out[f"{name}/speedup_vs_hicache"] = round(out[f"{name}/LRU_REACTIVE_HICACHE"]["step_latency_mean_s"] / k, 3)

@@ -49,3 +49,54 @@ def test_consumer_starts_before_the_load_finishes():
             for x in (j, c0, c1):
                 e.release(x)
         assert first < total / 4, (first, total)
+
+
+def test_engine_owned_counters_recycle_without_reset():
+    """layer_ready = NULL: the engine owns the counters (64 slots).  Counters only grow, so a
+    slot is reused without a reset and a consumer enqueued late on a recycled slot never
+    waits on the next job's progress.  More jobs than slots, each with a per-layer consumer."""
+    L = 4
+    with Engine(layers=L, kv_heads_total=8, head_dim=128, gpu_slots=2048, host_slots=2048) as e:
+        rng = np.random.default_rng(5)
+        cids = rng.integers(0, 2**63, size=256, dtype=np.uint64)
+        h = e.alloc(N.KVF_TIER_HOST, 256)
+        e.fill(N.KVF_TIER_HOST, h, cids)
+        d = e.alloc(N.KVF_TIER_DEVICE, 256)
+        for k in range(80):
+            j, _ = e.h2d_layered(h, d, None)
+            c = e.compute_begin()
+            for l in range(L):
+                e.compute_wait_job_layer(j, l)
+            e.compute_end(c)
+            e.wait(c)
+            e.release(c)
+            e.release(j)
+        assert e.checksum(N.KVF_TIER_DEVICE, d) == e.checksum(N.KVF_TIER_HOST, h)
+
+
+def test_engine_owned_counter_slots_are_bounded():
+    with Engine(layers=2, kv_heads_total=8, head_dim=128, gpu_slots=1024, host_slots=1024) as e:
+        h = e.alloc(N.KVF_TIER_HOST, 8)
+        d = e.alloc(N.KVF_TIER_DEVICE, 8)
+        jobs = [e.h2d_layered(h, d, None)[0] for _ in range(64)]
+        with pytest.raises(N.KvfError) as ei:
+            e.h2d_layered(h, d, None)
+        assert ei.value.code == N.KVF_E_TOO_LARGE
+        for j in jobs:
+            e.release(j)
+        j, _ = e.h2d_layered(h, d, None)  # a released slot is reusable
+        e.release(j)
+
+
+def test_wait_job_layer_on_a_plain_job_waits_for_the_whole_job():
+    with Engine(layers=2, kv_heads_total=8, head_dim=128, gpu_slots=1024, host_slots=1024) as e:
+        h = e.alloc(N.KVF_TIER_HOST, 64)
+        d = e.alloc(N.KVF_TIER_DEVICE, 64)
+        j = e.h2d(h, d)
+        c = e.compute_begin()
+        e.compute_wait_job_layer(j, 1)
+        e.compute_end(c)
+        e.wait(c)
+        assert e.query(j)
+        e.release(c)
+        e.release(j)

@@ -88,3 +88,14 @@ def test_wall_clock_compute_scale_runs_faster():
     assert bad == 0
     ref_res = [r for r in load_jsonl("sim_c1.jsonl") if r["t"] == "res"][0]
     assert res["makespan"] < 0.6 * ref_res["makespan"]
+
+
+def test_layered_gate_bytes_and_stall():
+    """§8f-1 in the driver: HiCache-gated prefills consume layer-pipelined loads (prefill layer
+    l waits only for layer l of its loads, on the GPU).  Bytes stay exact; the exposed stall
+    is no larger than with the whole-load gate."""
+    whole, _, _ = run_wall(policy="LRU_REACTIVE_HICACHE", **C2)
+    lay, trace, (checked, bad) = run_wall(policy="LRU_REACTIVE_HICACHE", layered_gate=1, **C2)
+    assert bad == 0 and lay["verify_failures"] == 0 and lay["verified_loads"] > 0
+    assert lay["reactive_jobs"] == whole["reactive_jobs"]
+    assert lay["stall_total_s"] <= whole["stall_total_s"] * 1.05 + 0.01
