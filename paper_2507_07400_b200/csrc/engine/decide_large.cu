@@ -38,14 +38,14 @@ struct BigTree {
     const uint64_t* tokens;
     const uint8_t* backed;
     uint32_t n;
-    uint64_t bpt;
 };
 
-struct BigReq {
+struct BigReq {  // lives in device memory (part of the uploaded blob): the graph is reusable
     uint64_t needed;
     int64_t floor;
     uint64_t cpu_used, cpu_cap;
     int32_t wa, offload, has_floor;
+    uint64_t bpt;  // bytes per token (per call: not baked into the graph)
 };
 
 __device__ __forceinline__ uint64_t time_order(double t) {
@@ -53,20 +53,23 @@ __device__ __forceinline__ uint64_t time_order(double t) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void big_stage(BigTree t, BigReq q, uint8_t* flags, uint32_t* blocked, uint32_t* vals) {
+__global__ void big_stage(BigTree t, const BigReq* __restrict__ q, uint8_t* flags, uint32_t* blocked, uint32_t* vals) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
-        const uint64_t bytes = t.tokens[i] * t.bpt;
-        const bool cpu_room = q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap;
-        const bool selfok = i > 0 && t.lock[i] == 0 && t.status[i] == 0 && (!q.has_floor || t.rank[i] > q.floor);
-        const bool releases = !q.offload || t.backed[i] || !cpu_room;
+        const uint64_t bytes = t.tokens[i] * q->bpt;
+        const bool cpu_room = q->cpu_cap == 0 || q->cpu_used + bytes <= q->cpu_cap;
+        const bool selfok =
+            i > 0 && t.lock[i] == 0 && t.status[i] == 0 && (!q->has_floor || t.rank[i] > q->floor);
+        const bool releases = !q->offload || t.backed[i] || !cpu_room;
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
         blocked[i] = 0;
         vals[i] = i;
     }
 }
 
-// keys[k] = word `w` of node vals[k]'s `before` key (ascending = earlier)
-__global__ void big_gather_key(BigTree t, const uint8_t* flags, const uint32_t* vals, uint64_t* keys, int w) {
+// keys[k] = word `w` of node vals[k]'s `before` key (ascending = earlier).  Only the relative
+// order of candidates matters downstream (ord is read for R nodes only), so non-candidates
+// need no extra pass to sort last.
+__global__ void big_gather_key(BigTree t, const uint32_t* vals, uint64_t* keys, int w) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
         const uint32_t i = vals[k];
         uint64_t key;
@@ -74,8 +77,7 @@ __global__ void big_gather_key(BigTree t, const uint8_t* flags, const uint32_t* 
             case 0: key = t.id[i]; break;
             case 1: key = t.seq[i]; break;
             case 2: key = time_order(t.time[i]); break;
-            case 3: key = ~(static_cast<uint64_t>(t.rank[i]) ^ 0x8000000000000000ull); break;  // rank desc
-            default: key = (flags[i] & 1) ? 0 : 1;                                             // candidates first
+            default: key = ~(static_cast<uint64_t>(t.rank[i]) ^ 0x8000000000000000ull); break;  // rank desc
         }
         keys[k] = key;
     }
@@ -120,33 +122,36 @@ __global__ void big_eff(BigTree t, const uint8_t* flags, const int32_t* ord, int
     }
 }
 
+// victim key (eff asc, depth desc) in 16 + log2(n) + 1 bits; non-R nodes sort last
 __global__ void big_victim_keys(BigTree t, const uint8_t* flags, const int32_t* eff, uint64_t* keys, uint32_t* vals) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
-        keys[i] = (flags[i] & 4) ? (static_cast<uint64_t>(static_cast<uint32_t>(eff[i])) << 32) |
-                                       (0xFFFFFFFFu - static_cast<uint32_t>(t.depth[i]))
+        keys[i] = (flags[i] & 4) ? (static_cast<uint64_t>(static_cast<uint32_t>(eff[i])) << 16) |
+                                       (0xFFFFu - static_cast<uint32_t>(t.depth[i]))
                                  : ~0ull;
         vals[i] = i;
     }
 }
 
-__global__ void big_bytes(BigTree t, const uint64_t* keys, const uint32_t* vals, uint64_t* bytes) {
+__global__ void big_bytes(BigTree t, const BigReq* __restrict__ q, const uint64_t* keys, const uint32_t* vals,
+                          uint64_t* bytes) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x)
-        bytes[k] = keys[k] == ~0ull ? 0 : t.tokens[vals[k]] * t.bpt;
+        bytes[k] = keys[k] == ~0ull ? 0 : t.tokens[vals[k]] * q->bpt;
 }
 
-// victim k is popped iff the bytes freed before it are < needed (radix_cache.cpp:335)
-__global__ void big_cut(BigTree t, BigReq q, const uint64_t* keys, const uint32_t* vals, const uint64_t* before,
-                        int32_t* out_idx, uint8_t* out_act, unsigned long long* header) {
+// victim k is popped iff the bytes freed before it are < needed (radix_cache.cpp:335);
+// idx / action go straight to mapped pinned host memory (posted writes, no D2H copy)
+__global__ void big_cut(BigTree t, const BigReq* __restrict__ q, const uint64_t* keys, const uint32_t* vals,
+                        const uint64_t* before, int32_t* out_idx, uint8_t* out_act, unsigned long long* header) {
     uint64_t imm = 0, pend = 0;
     uint32_t cnt = 0;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
-        if (keys[k] == ~0ull || before[k] >= q.needed) continue;
+        if (keys[k] == ~0ull || before[k] >= q->needed) continue;
         const uint32_t v = vals[k];
-        const uint64_t bytes = t.tokens[v] * t.bpt;
+        const uint64_t bytes = t.tokens[v] * q->bpt;
         uint8_t act;
-        if (!q.offload) act = KVF_ACT_REMOVE;
+        if (!q->offload) act = KVF_ACT_REMOVE;
         else if (t.backed[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
-        else if (!(q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap)) act = KVF_ACT_REMOVE;
+        else if (!(q->cpu_cap == 0 || q->cpu_used + bytes <= q->cpu_cap)) act = KVF_ACT_REMOVE;
         else act = KVF_ACT_OFFLOAD;
         out_idx[k] = static_cast<int32_t>(v);
         out_act[k] = act;
@@ -172,6 +177,21 @@ T* take(char*& p, size_t count) {
     return r;
 }
 
+// Bucketed size: n rounded up to a quarter of its octave (<= 25 % padding), so a captured
+// graph serves every tree size in the bucket.
+uint32_t bucket(uint32_t n) {
+    uint32_t p = 1;
+    while (p * 2 <= n) p *= 2;
+    const uint32_t step = std::max<uint32_t>(1024, p / 4);
+    return (n + step - 1) / step * step;
+}
+
+uint32_t bits_for(uint32_t x) {  // bits to hold 0..x
+    uint32_t b = 0;
+    while ((1ull << b) <= x) ++b;
+    return b;
+}
+
 }  // namespace
 
 namespace kvf_impl {
@@ -179,111 +199,141 @@ namespace kvf_impl {
 int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
                         uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend) {
     const uint32_t n = t->n;
+    const uint32_t np = bucket(n);
+    const bool wa = q->workflow_aware != 0;
     cudaStream_t s = e->s_dec;
-    // CUB scratch sizes for n items
     size_t sort_tmp = 0, scan_tmp = 0;
     KVF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint64_t*>(nullptr),
                                              static_cast<uint64_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                             static_cast<uint32_t*>(nullptr), static_cast<int>(n), 0, 64, s));
+                                             static_cast<uint32_t*>(nullptr), static_cast<int>(np), 0, 64, s));
     KVF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, static_cast<uint64_t*>(nullptr),
-                                           static_cast<uint64_t*>(nullptr), static_cast<int>(n), s));
-    const size_t in_bytes = static_cast<size_t>(n) * (8 * 5 + 4 * 2 + 2 + 2) + 16 * 256;
-    const size_t work_bytes = static_cast<size_t>(n) * (1 + 4 + 4 + 4 + 8 * 2 + 4 * 2 + 8 * 2 + 4 + 1) +
-                              sort_tmp + scan_tmp + 64 * 256;
-    const size_t out_host = 256 + static_cast<size_t>(n) * 5 + 512;
-    int rc = e->ws_big.ensure(in_bytes + work_bytes, in_bytes + out_host);
+                                           static_cast<uint64_t*>(nullptr), static_cast<int>(np), s));
+    const size_t in_bytes = 256 + static_cast<size_t>(np) * (8 * 5 + 4 * 2 + 2 + 2) + 16 * 256;
+    const size_t out_bytes = 256 + static_cast<size_t>(np) * 5 + 2 * 256;
+    const size_t work_bytes = static_cast<size_t>(np) * (1 + 4 + 4 + 4 + 8 * 2 + 4 * 2 + 8 * 2) + sort_tmp +
+                              scan_tmp + 64 * 256;
+    const void* old_dev = e->ws_big.dev;
+    const void* old_host = e->ws_big.host;
+    int rc = e->ws_big.ensure(in_bytes + work_bytes, in_bytes + out_bytes);
     if (rc) return rc;
-    // ---- pack + one H2D ----
+    if (e->ws_big.dev != old_dev || e->ws_big.host != old_host) {  // graphs bake the old pointers
+        for (auto& kv : e->big_graphs) cudaGraphExecDestroy(kv.second.exec);
+        e->big_graphs.clear();
+    }
+    // ---- pack the SoA (+ padding nodes that are never candidates) and the request ----
     char* h = static_cast<char*>(e->ws_big.host);
     char* hp = h;
-    std::memcpy(take<int64_t>(hp, n), t->rank, n * 8ull);
-    std::memcpy(take<double>(hp, n), t->time, n * 8ull);
-    std::memcpy(take<uint64_t>(hp, n), t->seq, n * 8ull);
-    std::memcpy(take<uint64_t>(hp, n), t->id, n * 8ull);
-    std::memcpy(take<uint64_t>(hp, n), t->tokens, n * 8ull);
-    std::memcpy(take<int32_t>(hp, n), t->parent, n * 4ull);
-    std::memcpy(take<int32_t>(hp, n), t->lock, n * 4ull);
-    std::memcpy(take<uint16_t>(hp, n), t->depth, n * 2ull);
-    std::memcpy(take<uint8_t>(hp, n), t->status, n);
-    std::memcpy(take<uint8_t>(hp, n), t->backed, n);
+    BigReq* hreq = take<BigReq>(hp, 1);
+    *hreq = BigReq{q->needed,       q->floor,        q->cpu_used,  q->cpu_capacity, q->workflow_aware,
+                   q->offload_mode, q->has_floor, t->bytes_per_token};
+    auto put = [&](auto* src, size_t elem, int fill) {
+        char* dst = hp;
+        std::memcpy(dst, src, n * elem);
+        std::memset(dst + n * elem, fill, (np - n) * elem);
+        hp += (np * elem + 255) & ~size_t(255);
+    };
+    put(t->rank, 8, 0);
+    put(t->time, 8, 0);
+    put(t->seq, 8, 0);
+    put(t->id, 8, 0);
+    put(t->tokens, 8, 0);
+    put(t->parent, 4, 0xFF);  // parent -1: walks stop at once
+    put(t->lock, 4, 0);
+    put(t->depth, 2, 0);
+    put(t->status, 1, 2);     // not IN_GPU: never a candidate, never R
+    put(t->backed, 1, 0);
     const size_t used = static_cast<size_t>(hp - h);
-    char* d = static_cast<char*>(e->ws_big.dev);
-    char* dp = d;
-    BigTree bt;
-    bt.rank = take<int64_t>(dp, n);
-    bt.time = take<double>(dp, n);
-    bt.seq = take<uint64_t>(dp, n);
-    bt.id = take<uint64_t>(dp, n);
-    bt.tokens = take<uint64_t>(dp, n);
-    bt.parent = take<int32_t>(dp, n);
-    bt.lock = take<int32_t>(dp, n);
-    bt.depth = take<uint16_t>(dp, n);
-    bt.status = take<uint8_t>(dp, n);
-    bt.backed = take<uint8_t>(dp, n);
-    bt.n = n;
-    bt.bpt = t->bytes_per_token;
-    uint8_t* flags = take<uint8_t>(dp, n);
-    uint32_t* blocked = take<uint32_t>(dp, n);
-    int32_t* ord = take<int32_t>(dp, n);
-    int32_t* eff = take<int32_t>(dp, n);
-    uint64_t* keys_a = take<uint64_t>(dp, n);
-    uint64_t* keys_b = take<uint64_t>(dp, n);
-    uint32_t* vals_a = take<uint32_t>(dp, n);
-    uint32_t* vals_b = take<uint32_t>(dp, n);
-    uint64_t* bytes = take<uint64_t>(dp, n);
-    uint64_t* before = take<uint64_t>(dp, n);
-    int32_t* d_idx = take<int32_t>(dp, n);
-    uint8_t* d_act = take<uint8_t>(dp, n);
-    unsigned long long* d_hdr = take<unsigned long long>(dp, 4);
-    void* sort_scratch = take<uint8_t>(dp, sort_tmp);
-    void* scan_scratch = take<uint8_t>(dp, scan_tmp);
-    BigReq rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
-    const uint32_t threads = 256;
-    const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((n + threads - 1) / threads, e->sm_count * 8ull));
-    KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, s));
-    KVF_CUDA(cudaMemsetAsync(d_hdr, 0, 32, s));
+    char* hout = h + ((used + 255) & ~size_t(255));
+    unsigned long long* hhdr = reinterpret_cast<unsigned long long*>(hout);
+    char* hout_dev = static_cast<char*>(e->ws_big.host_dev) + (hout - h);
+    int32_t* o_idx = reinterpret_cast<int32_t*>(hout_dev + 256);
+    uint8_t* o_act = reinterpret_cast<uint8_t*>(hout_dev + 256 + ((np * 4ull + 255) & ~255ull));
+
+    const uint64_t key = (static_cast<uint64_t>(np) << 1) | (wa ? 1u : 0u);
+    auto git = e->big_graphs.find(key);
+    if (git == e->big_graphs.end()) {
+        // ---- capture the whole device-wide sequence once per (bucket, policy) ----
+        char* d = static_cast<char*>(e->ws_big.dev);
+        char* dp = d;
+        const BigReq* dreq = take<BigReq>(dp, 1);
+        BigTree bt;
+        bt.rank = take<int64_t>(dp, np);
+        bt.time = take<double>(dp, np);
+        bt.seq = take<uint64_t>(dp, np);
+        bt.id = take<uint64_t>(dp, np);
+        bt.tokens = take<uint64_t>(dp, np);
+        bt.parent = take<int32_t>(dp, np);
+        bt.lock = take<int32_t>(dp, np);
+        bt.depth = take<uint16_t>(dp, np);
+        bt.status = take<uint8_t>(dp, np);
+        bt.backed = take<uint8_t>(dp, np);
+        bt.n = np;
+        uint8_t* flags = take<uint8_t>(dp, np);
+        uint32_t* blocked = take<uint32_t>(dp, np);
+        int32_t* ord = take<int32_t>(dp, np);
+        int32_t* eff = take<int32_t>(dp, np);
+        uint64_t* keys_a = take<uint64_t>(dp, np);
+        uint64_t* keys_b = take<uint64_t>(dp, np);
+        uint32_t* vals_a = take<uint32_t>(dp, np);
+        uint32_t* vals_b = take<uint32_t>(dp, np);
+        uint64_t* bytes = take<uint64_t>(dp, np);
+        uint64_t* before = take<uint64_t>(dp, np);
+        unsigned long long* d_hdr = take<unsigned long long>(dp, 4);
+        void* sort_scratch = take<uint8_t>(dp, sort_tmp);
+        void* scan_scratch = take<uint8_t>(dp, scan_tmp);
+        const uint32_t threads = 256;
+        const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((np + threads - 1) / threads, e->sm_count * 8ull));
+        cudaGraph_t g = nullptr;
+        KVF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(d_hdr, 0, 32, s);
+        big_stage<<<grid, threads, 0, s>>>(bt, dreq, flags, blocked, vals_a);
+        for (int w = 0; w < (wa ? 4 : 3); ++w) {  // stable LSD: id, seq, time, [rank desc]
+            big_gather_key<<<grid, threads, 0, s>>>(bt, vals_a, keys_a, w);
+            cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
+                                            static_cast<int>(np), 0, 64, s);
+            std::swap(vals_a, vals_b);
+        }
+        big_ord<<<grid, threads, 0, s>>>(np, vals_a, ord);
+        big_blocked<<<grid, threads, 0, s>>>(bt, flags, blocked);
+        big_r_init<<<grid, threads, 0, s>>>(np, flags, blocked, ord, eff);
+        big_eff<<<grid, threads, 0, s>>>(bt, flags, ord, eff);
+        big_victim_keys<<<grid, threads, 0, s>>>(bt, flags, eff, keys_a, vals_a);
+        cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b, static_cast<int>(np),
+                                        0, static_cast<int>(17 + bits_for(np)), s);
+        big_bytes<<<grid, threads, 0, s>>>(bt, dreq, keys_b, vals_b, bytes);
+        cub::DeviceScan::ExclusiveSum(scan_scratch, scan_tmp, bytes, before, static_cast<int>(np), s);
+        big_cut<<<grid, threads, 0, s>>>(bt, dreq, keys_b, vals_b, before, o_idx, o_act, d_hdr);
+        cudaMemcpyAsync(hhdr, d_hdr, 32, cudaMemcpyDeviceToHost, s);
+        const cudaError_t cap = cudaStreamEndCapture(s, &g);
+        if (cap != cudaSuccess) return cuda_error(cap, "K5 graph capture");
+        BigGraph bg;
+        const cudaError_t inst = cudaGraphInstantiate(&bg.exec, g, 0);
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(g, nodes.data(), &nn);
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++bg.kernels;
+        }
+        cudaGraphDestroy(g);
+        if (inst != cudaSuccess) return cuda_error(inst, "K5 graph instantiate");
+        git = e->big_graphs.emplace(key, bg).first;
+    }
     KVF_CUDA(cudaEventRecord(e->dec_start, s));
-    big_stage<<<grid, threads, 0, s>>>(bt, rq, flags, blocked, vals_a);
-    // stable LSD passes: id, seq, time, [rank desc], candidate bit
-    const int words[] = {0, 1, 2, 3, 4};
-    uint32_t launches = 1;
-    for (int w : words) {
-        if (w == 3 && !q->workflow_aware) continue;
-        big_gather_key<<<grid, threads, 0, s>>>(bt, flags, vals_a, keys_a, w);
-        KVF_CUDA(cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
-                                                 static_cast<int>(n), 0, w == 4 ? 1 : 64, s));
-        std::swap(vals_a, vals_b);
-        launches += 2;
-    }
-    big_ord<<<grid, threads, 0, s>>>(n, vals_a, ord);
-    big_blocked<<<grid, threads, 0, s>>>(bt, flags, blocked);
-    big_r_init<<<grid, threads, 0, s>>>(n, flags, blocked, ord, eff);
-    big_eff<<<grid, threads, 0, s>>>(bt, flags, ord, eff);
-    big_victim_keys<<<grid, threads, 0, s>>>(bt, flags, eff, keys_a, vals_a);
-    KVF_CUDA(cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
-                                             static_cast<int>(n), 0, 64, s));
-    big_bytes<<<grid, threads, 0, s>>>(bt, keys_b, vals_b, bytes);
-    KVF_CUDA(cub::DeviceScan::ExclusiveSum(scan_scratch, scan_tmp, bytes, before, static_cast<int>(n), s));
-    big_cut<<<grid, threads, 0, s>>>(bt, rq, keys_b, vals_b, before, d_idx, d_act, d_hdr);
-    KVF_CUDA(cudaGetLastError());
+    KVF_CUDA(cudaGraphLaunch(git->second.exec, s));
     KVF_CUDA(cudaEventRecord(e->dec_stop, s));
-    launches += 9;
-    e->stats.kernel_launches += launches;
+    e->stats.kernel_launches += git->second.kernels;
     e->stats.decisions++;
-    // ---- one D2H: header, then the victim prefix ----
-    char* ho = h + ((used + 255) & ~size_t(255));
-    KVF_CUDA(cudaMemcpyAsync(ho, d_hdr, 32, cudaMemcpyDeviceToHost, s));
     KVF_CUDA(cudaStreamSynchronize(s));
-    const uint64_t* hdr = reinterpret_cast<const uint64_t*>(ho);
-    const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
-    if (cnt) {
-        KVF_CUDA(cudaMemcpyAsync(out_idx, d_idx, cnt * 4ull, cudaMemcpyDeviceToHost, s));
-        KVF_CUDA(cudaMemcpyAsync(out_action, d_act, cnt, cudaMemcpyDeviceToHost, s));
-        KVF_CUDA(cudaStreamSynchronize(s));
-    }
+    const uint32_t cnt = static_cast<uint32_t>(hhdr[0]);
+    if (cnt > n) return set_error(KVF_E_INTERNAL, "device-wide K5: victim count beyond the tree");
+    std::memcpy(out_idx, hout + 256, cnt * 4ull);
+    std::memcpy(out_action, hout + 256 + ((np * 4ull + 255) & ~255ull), cnt);
     *out_count = cnt;
-    *out_imm = hdr[1];
-    *out_pend = hdr[2];
+    *out_imm = hhdr[1];
+    *out_pend = hhdr[2];
     return KVF_OK;
 }
 

@@ -792,6 +792,7 @@ int kvf_engine_destroy(kvf_engine* e) {
         if (s) cudaStreamDestroy(s);
     e->ws_dev.release();
     e->ws_dec.release();
+    for (auto& kv : e->big_graphs) cudaGraphExecDestroy(kv.second.exec);
     e->ws_big.release();
     if (e->d_checksum) cudaFree(e->d_checksum);
     if (e->d_layer_ctr) cudaFree(e->d_layer_ctr);

@@ -62,7 +62,12 @@ struct Job {
     uint32_t lr_base = 0, lr_tpl = 0;
 };
 
-constexpr uint32_t kLayerSlots = 64;  // concurrent layered loads with engine-owned counters
+constexpr uint32_t kLayerSlots = 64;
+
+struct BigGraph {  // device-wide K5 captured once per (bucketed size, policy)
+    cudaGraphExec_t exec = nullptr;
+    uint32_t kernels = 0;
+};  // concurrent layered loads with engine-owned counters
 
 struct Workspace {  // grow-only device + pinned staging buffers
     void* dev = nullptr;
@@ -107,6 +112,7 @@ struct kvf_engine {
     kvf_impl::Workspace ws_dev;  // fill / checksum / read staging (s_dev)
     kvf_impl::Workspace ws_dec;  // decision kernels (s_dec)
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
+    std::map<uint64_t, kvf_impl::BigGraph> big_graphs;  // key: bucket << 1 | workflow_aware
 
     uint64_t* d_checksum = nullptr;
     uint32_t* d_layer_ctr = nullptr;       // [kLayerSlots][layers] landed-tile counters

@@ -228,6 +228,16 @@ TEST("event queue: (time, push order) total order") {
     CHECK(!c.idle(1.0));
     CHECK_APPROX(c.busy_integral(1.0), 1.0);
     CHECK(c.idle(2.0));
+    // wall clock: a booked occupation that really ended early / late
+    ComputeClock w;
+    w.occupy(0, 2);
+    w.finish_at(1.5);
+    CHECK(w.idle(1.5));
+    CHECK_APPROX(w.busy_integral(3.0), 1.5);
+    w.occupy(3.0, 4.0);
+    w.finish_at(4.5);
+    CHECK(!w.idle(4.2));
+    CHECK_APPROX(w.busy_integral(5.0), 3.0);
 }
 
 // ------------------------------------------------------------- radix tree ---------------
@@ -391,6 +401,15 @@ TEST("tier ledger: timing follows bandwidth, efficiency and setup latency") {
     CHECK(n->cpu_backed);
     CHECK(!tier.load_completion_for_node(n->id).has_value());
     tier.audit(cache);
+}
+
+TEST("tier ledger: measured / wall-clock timing need the GPU engine (no CPU path)") {
+    EventQueue ev;
+    TierManager tier(4u << 20, 0, flat_cost(), ev);
+    EXPECT_CODE(tier.set_timing(TransferTiming::Measured), ErrorCode::NoDevice);
+    EXPECT_CODE(tier.set_timing(TransferTiming::WallClock), ErrorCode::NoDevice);
+    CHECK(tier.timing() == TransferTiming::Modeled);
+    CHECK(tier.inflight_ids().empty());
 }
 
 TEST("tier ledger: per-direction FIFO channels, full duplex across directions") {

@@ -195,3 +195,52 @@ def test_k5_victims_match_reference(eng, fixture):
         got = [(int(ta.id[v]), int(ta.tokens[v]) * ta.bpt, 0 if a == 0 else 1) for v, a in zip(idx, act)]
         assert got == [tuple(v) for v in c["victims"]], (fixture, c["case"])
         assert (imm, pend) == (c["immediate"], c["pending"])
+
+
+@pytest.mark.parametrize("geom", [
+    dict(layers=1, kv_heads_total=1, kv_heads_local=1, head_offset=0, head_dim=4),     # 8 B/token-plane: uint2 path
+    dict(layers=2, kv_heads_total=8, kv_heads_local=1, head_offset=5, head_dim=128),   # G = 8 shard, head 5
+    dict(layers=3, kv_heads_total=8, kv_heads_local=2, head_offset=6, head_dim=64),    # G = 4 shard, odd layers
+    dict(layers=80, kv_heads_total=8, kv_heads_local=1, head_offset=7, head_dim=128),  # Llama-3-70B, G = 8
+])
+def test_shard_geometries_bit_exact(geom):
+    """Every K1/K2/K3 path over shard geometries (head offsets, 8-byte token planes, odd layer
+    counts) against the oracle's payload restatement of the same shard; runs end on the last
+    slot of each pool."""
+    torch = pytest.importorskip("torch")
+    slots = 1024
+    with Engine(gpu_slots=slots, host_slots=slots, **geom) as e:
+        rng = np.random.default_rng(geom["layers"] * 31 + geom["head_offset"])
+        ntok = 300
+        cids = rand_cids(rng, ntok)
+        pre = e.alloc(N.KVF_TIER_HOST, slots - ntok)     # the node ends on the last host slot
+        h = e.alloc(N.KVF_TIER_HOST, ntok)
+        assert h[-1][0] + h[-1][1] == slots
+        e.fill(N.KVF_TIER_HOST, h, cids)
+        want = expected_bytes(e, cids)
+        assert np.array_equal(e.read(N.KVF_TIER_HOST, h), want)
+        d = fragment(e, N.KVF_TIER_DEVICE, ntok, rng, pieces=7)
+        for mode in MODES:
+            e.set_copy_mode(mode)
+            j = e.h2d(h, d)
+            e.wait(j)
+            e.release(j)
+            assert np.array_equal(e.read(N.KVF_TIER_DEVICE, d), want), mode
+        e.set_copy_mode(N.KVF_COPY_SM_VEC)
+        j, _ = e.h2d_layered(h, d, None)
+        e.wait(j)
+        e.release(j)
+        assert np.array_equal(e.read(N.KVF_TIER_DEVICE, d), want)
+        stage = torch.zeros(ntok * e.token_bytes, dtype=torch.uint8, device="cuda")
+        j = e.dev_gather(d, stage.data_ptr())
+        e.wait(j)
+        e.release(j)
+        torch.cuda.synchronize()
+        assert np.array_equal(stage.cpu().numpy(), want)
+        e.free(N.KVF_TIER_HOST, pre)
+        h2 = fragment(e, N.KVF_TIER_HOST, ntok, rng, pieces=5)
+        j = e.d2h(d, h2)
+        e.wait(j)
+        e.release(j)
+        assert np.array_equal(e.read(N.KVF_TIER_HOST, h2), want)
+        assert e.checksum(N.KVF_TIER_HOST, h2) == e.checksum(N.KVF_TIER_DEVICE, d) == e.payload_checksum(cids)
