@@ -129,7 +129,7 @@ def run_ours(args, rank, world, local):
     import torch.distributed as dist
 
     from paper_2507_07400_b200 import _native as N
-    from paper_2507_07400_b200.engine import Engine
+    from paper_2507_07400_b200.engine import Engine, device_numa_node
     from paper_2507_07400_b200.sim import Sim
 
     # KVF_BENCH_SAME_DEVICE=1 maps every rank to GPU 0 and uses gloo: a 1-GPU rehearsal of the
@@ -146,11 +146,14 @@ def run_ours(args, rank, world, local):
     heads, bpt, budget = sp.kv_heads_local, sp.bytes_per_token, sp.gpu_budget
     gpu_slots = budget // bpt
     suffix = DYN + OUT
+    numa = device_numa_node(local)
     peaks, peak_src = measured_peaks()
     pcie = ce_h2d_peak(torch)
 
     # ---- kernel-level steady-state replay (value, roofline) --------------------------
-    eng = Engine(**sp.engine_kwargs(), gpu_slots=gpu_slots, host_slots=4 * FIXED + 64 * suffix, device=local)
+    # host pool pinned on the GPU's own NUMA node: with N GPUs each rank streams from local DRAM
+    eng = Engine(**sp.engine_kwargs(), gpu_slots=gpu_slots, host_slots=4 * FIXED + 64 * suffix, device=local,
+                 numa_node=N.KVF_NUMA_AUTO)
     rng = np.random.default_rng(1)
     fixed_host = [eng.alloc(N.KVF_TIER_HOST, FIXED) for _ in range(4)]
     for r in fixed_host:
@@ -201,7 +204,8 @@ def run_ours(args, rank, world, local):
     eng.close()
 
     # ---- e2e: the full workflow through the public API ---------------------------------
-    sim = Sim(fixed=FIXED, dyn=DYN, out=OUT, gpu_cap=budget, bytes_per_token=bpt, device=local, **sp.engine_kwargs())
+    sim = Sim(fixed=FIXED, dyn=DYN, out=OUT, gpu_cap=budget, bytes_per_token=bpt, device=local,
+              numa_node=N.KVF_NUMA_AUTO, **sp.engine_kwargs())
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
@@ -250,7 +254,8 @@ def run_ours(args, rank, world, local):
         "config": {"workload": WORKLOAD, "kv_bytes_per_token": BPT_FULL, "gpu_budget_bytes": BUDGET_FULL,
                    "step": "1 x 8192-token prefetch (K1) || 1 x 128-token write-back (K2)",
                    "prefetch_bytes_per_step": pre_bytes * world, "l2": "inputs larger than L2 (1 GiB per prefetch)",
-                   "parallelism": f"kv-head shard x{world} (no data-path collective)", "pcie_mode": "sm_vec"},
+                   "parallelism": f"kv-head shard x{world} (no data-path collective)", "pcie_mode": "sm_vec",
+                   "host_numa_node": numa},
         "roofline": {"bound": "pcie_h2d", "kernel": "kvf_copy_vec_kernel (K1 H2D gather)",
                      "achieved": round(achieved, 3), "peak": round(pcie["h2d"], 3), "unit": "GB/s",
                      "frac": round(achieved / pcie["h2d"], 4), "traffic": ncu_traffic(),

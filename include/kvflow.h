@@ -90,7 +90,8 @@ typedef struct {
     uint32_t pcie_ctas;       /* grid for K1/K2 (0 = default)                          */
     uint32_t pcie_mode;       /* KVF_COPY_* for K1/K2                                  */
     uint32_t hbm_ctas;        /* grid for K3 (0 = default: 4 per SM)                   */
-    int32_t host_numa_node;   /* -1: no binding; else mbind the host pool to this node */
+    int32_t host_numa_node;   /* -1: no binding; KVF_NUMA_AUTO (-2): the GPU's own node
+                                 (sysfs of its PCI device); else mbind the host pool there */
 } kvf_engine_config;
 
 typedef struct {
@@ -102,6 +103,9 @@ typedef struct {
 const char* kvf_last_error(void);
 const char* kvf_version(void);
 int kvf_device_count(int32_t* out);
+#define KVF_NUMA_AUTO (-2)
+/* NUMA node of a GPU's PCI device (-1 when the platform does not say). */
+int kvf_device_numa_node(int32_t device, int32_t* node);
 int kvf_engine_create(const kvf_geometry* geom, const kvf_engine_config* cfg, kvf_engine** out);
 int kvf_engine_destroy(kvf_engine* e);
 /* bytes one token occupies in one plane on this shard, and across all planes */
@@ -131,6 +135,13 @@ int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint
 int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* dev_runs,
                     uint32_t n_dev);
 
+/* K2 for several nodes in ONE launch (small-node write-back batching):
+ * job k moves dev_runs[off_k .. off_k + dev_counts[k]) -> host_runs[...host_counts[k]), the
+ * run lists concatenated in job order.  Every job keeps its own id and events (all complete
+ * when the shared launch does); the batch is validated before any job is created.
+ * Reference: one tier_manager.cpp:48-59 begin_offload per node of an evict call. */
+int kvf_d2h_scatter_batch(kvf_engine* e, uint32_t n_jobs, const uint64_t* job_ids, const kvf_run* dev_runs,
+                          const uint32_t* dev_counts, const kvf_run* host_runs, const uint32_t* host_counts);
 /* K1, layer-pipelined: tiles go plane-outermost, and each finished tile bumps
  * layer_ready[layer] (caller's device array of `layers` uint32, zeroed by the call); layer l
  * has landed when layer_ready[l] == *tiles_per_layer.  A consumer can start on layer l while
@@ -222,6 +233,7 @@ typedef struct {
     double decision_call_us;   /* K4+K5 host round trip (pack, H2D, kernel, D2H, sync)  */
     double k5_phase_ns[5];     /* K5 in-kernel phases: stage, sort, walks, victim sort, scan+out */
     double k5_phase_cycles[5]; /* the same phases in SM cycles (clock64)                       */
+    uint64_t stale_errors;     /* non-sticky CUDA errors found pending at API entry (cleared) */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

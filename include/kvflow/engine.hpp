@@ -53,6 +53,9 @@ public:
     // layer-pipelined K1 with engine-owned per-layer landed counters
     void h2d_layered(uint64_t job, const RunList& host, const RunList& dev);
     void d2h(uint64_t job, const RunList& dev, const RunList& host);
+    // one K2 launch for several nodes (each job keeps its id and events)
+    void d2h_batch(const std::vector<uint64_t>& jobs, const std::vector<const RunList*>& dev,
+                   const std::vector<const RunList*>& host);
     bool query(uint64_t job);
     void wait(uint64_t job);
     float elapsed_ms(uint64_t job);

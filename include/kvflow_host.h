@@ -54,6 +54,7 @@ typedef struct {
     uint32_t compute_ctas;  /* wall clock: CTAs the compute emulation spins on (0 -> 128) */
     int32_t prefetch_retry; /* re-run the step-1 prefetch whenever a transfer lands */
     int32_t layered_gate;   /* wall clock: HiCache-gated prefills consume layer-pipelined loads */
+    int32_t d2h_unbatched;  /* 1: one K2 launch per write-back instead of one per evict call */
 } kvfh_sim_config;
 
 typedef struct {
@@ -72,6 +73,7 @@ typedef struct {
     uint64_t kernel_launches;
     uint64_t verified_loads, verify_failures;
     uint64_t audits;
+    uint64_t d2h_batches;     /* K2 batch launches (one per evict call with write-backs) */
     /* stalls (RequestTrace::stall_seconds, virtual seconds) over measured requests */
     double stall_total_s;
     uint64_t stalled_requests, measured_requests;

@@ -15,6 +15,7 @@ class SimConfig(C.Structure):
         ("pcie_mode", C.c_uint32), ("pcie_ctas", C.c_uint32), ("numa_node", C.c_int32), ("audit", C.c_int32),
         ("verify_loads", C.c_int32), ("timing", C.c_int32), ("clock", C.c_int32), ("compute_scale", C.c_double),
         ("compute_ctas", C.c_uint32), ("prefetch_retry", C.c_int32), ("layered_gate", C.c_int32),
+        ("d2h_unbatched", C.c_int32),
     ]
 
 
@@ -29,7 +30,8 @@ class SimResult(C.Structure):
         ("reactive_device_ms", C.c_double), ("offload_device_ms", C.c_double), ("fence_wait_us", C.c_double),
         ("priority_calls", C.c_uint64), ("evict_calls", C.c_uint64), ("priority_us", C.c_double),
         ("evict_us", C.c_double), ("kernel_launches", C.c_uint64), ("verified_loads", C.c_uint64),
-        ("verify_failures", C.c_uint64), ("audits", C.c_uint64), ("stall_total_s", C.c_double),
+        ("verify_failures", C.c_uint64), ("audits", C.c_uint64), ("d2h_batches", C.c_uint64),
+        ("stall_total_s", C.c_double),
         ("stalled_requests", C.c_uint64), ("measured_requests", C.c_uint64),
     ]
 

@@ -19,6 +19,7 @@ HOST_SO = os.path.join(PKG, "libkvflow_host.so")
 KVF_OK = 0
 KVF_TIER_DEVICE, KVF_TIER_HOST = 0, 1
 KVF_COPY_SM_VEC, KVF_COPY_SM_BULK, KVF_COPY_CE = 0, 1, 2
+KVF_NUMA_AUTO = -2
 KVF_E_INVALID_ARG, KVF_E_OUT_OF_HOST_SLOTS, KVF_E_NO_DEVICE, KVF_E_UNKNOWN_JOB, KVF_E_TOO_LARGE = 101, 102, 103, 104, 105
 
 
@@ -61,7 +62,7 @@ class Stats(C.Structure):
                 ("dev_bytes", C.c_uint64), ("h2d_jobs", C.c_uint64), ("d2h_jobs", C.c_uint64),
                 ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
                 ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5),
-                ("k5_phase_cycles", C.c_double * 5)]
+                ("k5_phase_cycles", C.c_double * 5), ("stale_errors", C.c_uint64)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature
@@ -69,6 +70,7 @@ _ENGINE_SIGS = {
     "kvf_last_error": (C.c_char_p, []),
     "kvf_version": (C.c_char_p, []),
     "kvf_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
+    "kvf_device_numa_node": (C.c_int, [C.c_int32, C.POINTER(C.c_int32)]),
     "kvf_engine_create": (C.c_int, [C.POINTER(Geometry), C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),
     "kvf_engine_destroy": (C.c_int, [C.c_void_p]),
     "kvf_engine_token_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -80,6 +82,8 @@ _ENGINE_SIGS = {
     "kvf_pool_ptr": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)]),
     "kvf_h2d_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32]),
     "kvf_d2h_scatter": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32]),
+    "kvf_d2h_scatter_batch": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(Run),
+                                        C.POINTER(C.c_uint32), C.POINTER(Run), C.POINTER(C.c_uint32)]),
     "kvf_dev_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.c_void_p]),
     "kvf_dev_scatter": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(Run), C.c_uint32]),
     "kvf_h2d_gather_layered": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32,

@@ -515,6 +515,7 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     if (!e || !parent || !out_rank || (m && (!bidx || !cand))) return set_error(KVF_E_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lk(e->mu);
     if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
+    clear_stale_error(e, __func__);
     if (n == 0) return KVF_OK;
     const auto t0 = std::chrono::steady_clock::now();
     for (uint32_t b = 0; b < m; ++b)
@@ -542,7 +543,7 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_copy ? used : 0);
-    if (smem > 48 * 1024 && !e->prio_attr_set) {
+    if (!e->prio_attr_set) {
         KVF_CUDA(cudaFuncSetAttribute(kvf_priority_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kPrioSmemNodes * 8 + kZeroCopyBytes + 64)));
         e->prio_attr_set = true;
@@ -566,6 +567,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
         return set_error(KVF_E_INVALID_ARG, "null argument");
     std::lock_guard<std::mutex> lk(e->mu);
     if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
+    clear_stale_error(e, __func__);
     const uint32_t n = t->n;
     *out_count = 0;
     *out_imm = *out_pend = 0;
@@ -620,14 +622,18 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     ReqDev rq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode, q->has_floor};
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, e->s_dec));
     const size_t smem = victim_smem(n, zero_copy ? used : 0);
-    if (smem > 48 * 1024 && !e->victim_attr_set) {  // per engine: attributes are per device
+    if (!e->victim_attr_set) {  // once per engine (attributes are per device); unconditional:
+                                 // the 48 KB default also counts the kernel's static shared memory
         KVF_CUDA(cudaFuncSetAttribute(kvf_victim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(victim_smem(kMaxNodesSingleCta))));
         e->victim_attr_set = true;
     }
     KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od);
-    KVF_CUDA(cudaGetLastError());
+    if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess)
+        return cuda_error(le, ("K5 launch (n=" + std::to_string(n) + " threads=" + std::to_string(victim_threads(n)) +
+                               " smem=" + std::to_string(smem) + " zero_copy=" + std::to_string(zero_copy) + ")")
+                                  .c_str());
     KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;

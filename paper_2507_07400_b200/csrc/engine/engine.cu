@@ -11,7 +11,9 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -157,6 +159,18 @@ void Workspace::release() {
     if (host) cudaFreeHost(host);
     dev = host = host_dev = nullptr;
     dev_bytes = host_bytes = 0;
+}
+
+// A non-sticky error left in the runtime's per-thread slot by an unchecked call elsewhere
+// (another engine's teardown, a caller's own CUDA use) must not be reported by the next
+// launch check of this call: take it out at entry, count it, optionally trace it
+// (KVF_TRACE_STALE=1).  Sticky errors (a faulted context) resurface at the next sync anyway.
+void clear_stale_error(kvf_engine* e, const char* fn) {
+    const cudaError_t stale = cudaGetLastError();
+    if (stale == cudaSuccess) return;
+    e->stats.stale_errors++;
+    static const bool trace = std::getenv("KVF_TRACE_STALE") != nullptr;
+    if (trace) std::fprintf(stderr, "kvflow: stale %s before %s\n", cudaGetErrorName(stale), fn);
 }
 
 int acquire_event(kvf_engine* e, cudaEvent_t* ev) {
@@ -674,7 +688,8 @@ uint32_t grid_for(const kvf_engine* e, uint64_t work, uint32_t threads) {
 #define KVF_GUARD(e) \
     if (!(e)) return set_error(KVF_E_INVALID_ARG, "null engine"); \
     std::lock_guard<std::mutex> _lk((e)->mu); \
-    if (cudaSetDevice((e)->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed")
+    if (cudaSetDevice((e)->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed"); \
+    kvf_impl::clear_stale_error(e, __func__)
 
 extern "C" {
 
@@ -686,6 +701,25 @@ int kvf_device_count(int32_t* out) {
     cudaError_t err = cudaGetDeviceCount(&n);
     if (err != cudaSuccess) n = 0;
     if (out) *out = n;
+    return KVF_OK;
+}
+
+int kvf_device_numa_node(int32_t device, int32_t* node) {
+    if (!node) return set_error(KVF_E_INVALID_ARG, "null node");
+    *node = -1;
+    char bus[32] = {0};
+    const cudaError_t err = cudaDeviceGetPCIBusId(bus, sizeof(bus), device);
+    if (err != cudaSuccess) return err == cudaErrorNoDevice || err == cudaErrorInvalidDevice
+                                       ? set_error(KVF_E_NO_DEVICE, "no CUDA device")
+                                       : cuda_error(err, "cudaDeviceGetPCIBusId");
+    for (char* c = bus; *c; ++c) *c = static_cast<char>(std::tolower(static_cast<unsigned char>(*c)));
+    const std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+    FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) return KVF_OK;  // unknown: -1
+    int v = -1;
+    if (std::fscanf(f, "%d", &v) != 1) v = -1;
+    std::fclose(f);
+    *node = v;
     return KVF_OK;
 }
 
@@ -726,12 +760,15 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
     }
     if (e->host_slots) {
         const size_t bytes = e->host_slots * e->token_bytes;
-        if (cfg->host_numa_node >= 0) {
+        int32_t numa = cfg->host_numa_node;
+        if (numa == KVF_NUMA_AUTO && kvf_device_numa_node(e->device, &numa) != KVF_OK) numa = -1;
+        if (numa >= 0) {
             // NUMA-local pinned shard: mmap, bind to the GPU's node, then pin + map.
             void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
             if (p == MAP_FAILED) return fail(set_error(KVF_E_OUT_OF_HOST_SLOTS, "mmap host pool"));
             unsigned long mask[16] = {0};
-            const int node = cfg->host_numa_node;
+            const int node = numa;
+            e->host_numa = numa;
             if (node < 1024) mask[node / 64] |= 1ul << (node % 64);
             syscall(SYS_mbind, p, bytes, 2 /*MPOL_BIND*/, mask, 1024ul, 0u);  // best effort
             e->host_pool = static_cast<char*>(p);
@@ -875,6 +912,53 @@ int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uin
                     uint32_t n_host) {
     KVF_GUARD(e);
     return transfer(e, job_id, KVF_TIER_DEVICE, dev_runs, n_dev, KVF_TIER_HOST, host_runs, n_host);
+}
+
+int kvf_d2h_scatter_batch(kvf_engine* e, uint32_t n_jobs, const uint64_t* job_ids, const kvf_run* dev_runs,
+                          const uint32_t* dev_counts, const kvf_run* host_runs, const uint32_t* host_counts) {
+    KVF_GUARD(e);
+    if (n_jobs == 0) return KVF_OK;
+    if (!job_ids || !dev_counts || !host_counts) return set_error(KVF_E_INVALID_ARG, "null batch array");
+    // validate everything before any job exists: a bad entry leaves no half-issued batch
+    std::vector<Piece> pieces;
+    std::vector<uint64_t> bytes(n_jobs);
+    size_t od = 0, oh = 0;
+    for (uint32_t k = 0; k < n_jobs; ++k) {
+        if (e->jobs.count(job_ids[k])) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_ids[k]) + " already in use");
+        for (uint32_t q = 0; q < k; ++q)
+            if (job_ids[q] == job_ids[k]) return set_error(KVF_E_INVALID_ARG, "duplicate job id in batch");
+        const kvf_run* dr = dev_runs + od;
+        const kvf_run* hr = host_runs + oh;
+        if ((dev_counts[k] && !dev_runs) || (host_counts[k] && !host_runs)) return set_error(KVF_E_INVALID_ARG, "null run list");
+        uint64_t td = 0, th = 0;
+        if (!runs_valid(e, KVF_TIER_DEVICE, dr, dev_counts[k], &td) || !runs_valid(e, KVF_TIER_HOST, hr, host_counts[k], &th))
+            return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+        if (td != th) return set_error(KVF_E_INVALID_ARG, "source and destination token counts differ");
+        std::vector<Piece> mine;
+        merge_runs(dr, dev_counts[k], hr, host_counts[k], mine);
+        pieces.insert(pieces.end(), mine.begin(), mine.end());
+        bytes[k] = td * e->token_bytes;
+        od += dev_counts[k];
+        oh += host_counts[k];
+    }
+    std::vector<Job> js(n_jobs);
+    for (uint32_t k = 0; k < n_jobs; ++k) {
+        int rc = begin_job(e, job_ids[k], e->s_d2h, js[k]);
+        if (rc) return rc;
+    }
+    if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_d2h, e->dev_write_done, 0));
+    Endpoint src{e->dev_pool, e->dev_slots * e->tpb, false};
+    Endpoint dst{e->host_pool_dev, e->host_slots * e->tpb, true};
+    int rc = launch_copy(e, e->s_d2h, src, dst, pieces, e->cfg.pcie_mode, e->cfg.pcie_ctas);  // one K2 for all
+    if (rc) return rc;
+    for (uint32_t k = 0; k < n_jobs; ++k) {
+        js[k].bytes = bytes[k];
+        e->stats.d2h_bytes += bytes[k];
+        e->stats.d2h_jobs++;
+        rc = end_job(e, job_ids[k], js[k]);
+        if (rc) return rc;
+    }
+    return KVF_OK;
 }
 
 int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_runs, uint32_t n_host,

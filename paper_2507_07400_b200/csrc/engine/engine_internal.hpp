@@ -95,7 +95,8 @@ struct kvf_engine {
     char* host_pool = nullptr;      // host address
     char* host_pool_dev = nullptr;  // device-side address of the same memory
     uint64_t host_slots = 0;
-    bool host_registered = false;   // mmap+cudaHostRegister (NUMA-bound) vs cudaHostAlloc
+    bool host_registered = false;
+    int32_t host_numa = -1;         // node the host pool is bound to (-1: none)   // mmap+cudaHostRegister (NUMA-bound) vs cudaHostAlloc
     size_t host_map_bytes = 0;
 
     kvf_impl::SlotAllocator alloc[2];
@@ -125,6 +126,7 @@ struct kvf_engine {
 
 namespace kvf_impl {
 int acquire_event(kvf_engine* e, cudaEvent_t* ev);
+void clear_stale_error(kvf_engine* e, const char* fn);
 int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
                         uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend);
 void recycle_event(kvf_engine* e, cudaEvent_t ev);

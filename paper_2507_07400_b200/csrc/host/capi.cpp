@@ -178,6 +178,7 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
         }
         s->sim->wall.prefetch_retry = c->prefetch_retry != 0;
         s->sim->wall.layered_gate = c->layered_gate != 0;
+        if (c->d2h_unbatched) s->sim->tier().set_offload_batching(false);
         // record every transition, tagged with the event index (same stream as ref_trace)
         auto prev = s->sim->tier().transition_observer;
         kvfh_sim* raw = s.get();
@@ -280,6 +281,7 @@ int kvfh_sim_result_get(const kvfh_sim* s, kvfh_sim_result* r) {
         r->verified_loads = s->sim->verified_loads;
         r->verify_failures = s->sim->verify_failures;
         r->audits = s->audits;
+        r->d2h_batches = s->sim->tier().batched_launches();
         for (const RequestTrace& t : s->result.traces) {
             if (!t.measured) continue;
             r->measured_requests++;

@@ -89,6 +89,20 @@ void Engine::d2h(uint64_t job, const RunList& dev, const RunList& host) {
                              static_cast<uint32_t>(host.size())));
 }
 
+void Engine::d2h_batch(const std::vector<uint64_t>& jobs, const std::vector<const RunList*>& dev,
+                       const std::vector<const RunList*>& host) {
+    std::vector<Run> d, h;
+    std::vector<uint32_t> dc, hc;
+    for (size_t k = 0; k < jobs.size(); ++k) {
+        d.insert(d.end(), dev[k]->begin(), dev[k]->end());
+        h.insert(h.end(), host[k]->begin(), host[k]->end());
+        dc.push_back(static_cast<uint32_t>(dev[k]->size()));
+        hc.push_back(static_cast<uint32_t>(host[k]->size()));
+    }
+    KVF_CALL(kvf_d2h_scatter_batch(e_, static_cast<uint32_t>(jobs.size()), jobs.data(), d.data(), dc.data(), h.data(),
+                                   hc.data()));
+}
+
 bool Engine::query(uint64_t job) {
     int32_t done = 0;
     KVF_CALL(kvf_job_query(e_, job, &done));

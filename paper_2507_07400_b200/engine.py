@@ -19,6 +19,13 @@ def device_count() -> int:
     return n.value
 
 
+def device_numa_node(device: int) -> int:
+    """NUMA node of the GPU's PCI device (-1 if unknown)."""
+    n = C.c_int32()
+    N.check(N.engine_lib().kvf_device_numa_node(device, C.byref(n)))
+    return n.value
+
+
 class Engine:
     """One KV-movement engine = one GPU shard (HBM pool + pinned host pool + streams)."""
 
@@ -99,6 +106,18 @@ class Engine:
         N.check(self._lib.kvf_d2h_scatter(self.h, job, N.runs_array(dev_runs), len(dev_runs),
                                           N.runs_array(host_runs), len(host_runs)))
         return job
+
+    def d2h_batch(self, pairs, jobs=None):
+        """One K2 launch for several nodes: pairs = [(dev_runs, host_runs), ...]; returns job ids."""
+        jobs = jobs or [self.new_job() for _ in pairs]
+        n = len(pairs)
+        ids = (C.c_uint64 * max(1, n))(*jobs)
+        dc = (C.c_uint32 * max(1, n))(*[len(d) for d, _ in pairs])
+        hc = (C.c_uint32 * max(1, n))(*[len(h) for _, h in pairs])
+        dev = N.runs_array([r for d, _ in pairs for r in d])
+        host = N.runs_array([r for _, h in pairs for r in h])
+        N.check(self._lib.kvf_d2h_scatter_batch(self.h, n, ids, dev, dc, host, hc))
+        return jobs
 
     def h2d_layered(self, host_runs, dev_runs, layer_ready_ptr, job=None):
         """Layer-pipelined K1; returns (job, tiles_per_layer)."""

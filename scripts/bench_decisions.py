@@ -31,7 +31,7 @@ def tree_of(c):
 
 
 def main():
-    e = Engine(layers=32, kv_heads_total=8, head_dim=128, gpu_slots=8192 + 64, host_slots=8192 + 64)
+    e = Engine(layers=32, kv_heads_total=8, head_dim=128, gpu_slots=8192 + 256, host_slots=8192 + 256)
     h = e.alloc(N.KVF_TIER_HOST, 8192)
     d = e.alloc(N.KVF_TIER_DEVICE, 8192)
     cases = sorted(load_jsonl("evict_small.jsonl") + load_jsonl("evict_medium.jsonl"), key=lambda c: len(c["parent"]))
@@ -65,15 +65,23 @@ def main():
         row["cpu_restatement_us_incl_python"] = round((time.perf_counter() - w0) / reps * 1e6, 2)
         out.append(row)
     prio = sorted(load_jsonl("prio.jsonl"), key=lambda c: len(c["parent"]))
+    hb = e.alloc(N.KVF_TIER_HOST, 128)
+    db = e.alloc(N.KVF_TIER_DEVICE, 128)
     for c in (prio[0], prio[len(prio) // 2], prio[-1]):
         b = c["boundaries"]
-        s0 = e.stats()
-        for _ in range(reps):
-            e.priority(c["parent"], [x[0] for x in b], [int(x[1]) for x in b])
-        s1 = e.stats()
-        out.append({"k4_nodes": len(c["parent"]), "boundaries": len(b),
-                    "k4_kernel_us": round((s1["decision_kernel_ms"] - s0["decision_kernel_ms"]) / reps * 1e3, 2),
-                    "k4_call_us": round((s1["decision_call_us"] - s0["decision_call_us"]) / reps, 2)})
+        row = {"k4_nodes": len(c["parent"]), "boundaries": len(b)}
+        for load in ("idle", "busy_h2d", "busy_both"):
+            jobs = [] if load == "idle" else [e.h2d(h, d)] + ([e.d2h(db, hb)] if load == "busy_both" else [])
+            s0 = e.stats()
+            for _ in range(reps):
+                e.priority(c["parent"], [x[0] for x in b], [int(x[1]) for x in b])
+            s1 = e.stats()
+            for j in jobs:
+                e.wait(j)
+                e.release(j)
+            row[f"k4_kernel_us_{load}"] = round((s1["decision_kernel_ms"] - s0["decision_kernel_ms"]) / reps * 1e3, 2)
+            row[f"k4_call_us_{load}"] = round((s1["decision_call_us"] - s0["decision_call_us"]) / reps, 2)
+        out.append(row)
     print(json.dumps(out, indent=1))
 
 

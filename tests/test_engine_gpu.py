@@ -244,3 +244,83 @@ def test_shard_geometries_bit_exact(geom):
         e.release(j)
         assert np.array_equal(e.read(N.KVF_TIER_HOST, h2), want)
         assert e.checksum(N.KVF_TIER_HOST, h2) == e.checksum(N.KVF_TIER_DEVICE, d) == e.payload_checksum(cids)
+
+
+def test_d2h_batch_one_launch_bit_exact(eng):
+    """kvf_d2h_scatter_batch: several nodes' write-backs in one K2 launch, each job with its
+    own id / events, bytes exact; a bad entry rejects the whole batch before any job exists."""
+    rng = np.random.default_rng(21)
+    nodes = []
+    for ntok in (17, 128, 3, 200):
+        cids = rand_cids(rng, ntok)
+        d = fragment(eng, N.KVF_TIER_DEVICE, ntok, rng, pieces=3)
+        eng.fill(N.KVF_TIER_DEVICE, d, cids)
+        h = fragment(eng, N.KVF_TIER_HOST, ntok, rng, pieces=2)
+        nodes.append((d, h, cids))
+    l0 = eng.stats()["kernel_launches"]
+    jobs = eng.d2h_batch([(d, h) for d, h, _ in nodes])
+    assert eng.stats()["kernel_launches"] - l0 == 1
+    for j, (d, h, cids) in zip(jobs, nodes):
+        eng.wait(j)
+        assert eng.elapsed_ms(j) >= 0
+        eng.release(j)
+        assert np.array_equal(eng.read(N.KVF_TIER_HOST, h), expected_bytes(eng, cids))
+    d, h, _ = nodes[0]
+    with pytest.raises(N.KvfError):  # token counts differ in the 2nd entry
+        eng.d2h_batch([(d, h), (nodes[1][0], nodes[2][1])])
+    with pytest.raises(N.KvfError):  # duplicate job ids
+        eng.d2h_batch([(d, h), (d, h)], jobs=[77, 77])
+    j = eng.d2h_batch([(d, h)], jobs=[77])[0]  # nothing of the rejected batches was left behind
+    eng.wait(j)
+    eng.release(j)
+    for d, h, _ in nodes:
+        eng.free(N.KVF_TIER_DEVICE, d)
+        eng.free(N.KVF_TIER_HOST, h)
+
+
+def random_case(rng, n):
+    parent = [-1] + [int(rng.integers(0, i)) for i in range(1, n)]
+    status = [0] + [int(x) for x in rng.choice([0, 0, 0, 1], size=n - 1)]
+    return {
+        "parent": parent, "status": status,
+        "lock": [0] + [int(x) for x in rng.choice([0, 0, 0, 0, 1], size=n - 1)],
+        "rank": [int(x) for x in rng.choice([2**62 - 1, 2**61 - 1, 1, 2, 3, 5], size=n)],
+        "time": [float(x) for x in rng.integers(0, n // 3 + 1, size=n) * 0.25],  # ties on time
+        "seq": [int(x) for x in rng.integers(0, n // 2 + 1, size=n)],            # and on seq
+        "id": [int(x) for x in rng.permutation(n) + 1],
+        "tokens": [int(x) for x in rng.integers(1, 300, size=n)],
+        "backed": [int(x) for x in rng.integers(0, 2, size=n)],
+        "bpt": 1024, "policy": int(rng.integers(0, 2)), "mode": int(rng.integers(0, 2)),
+        "has_floor": int(rng.integers(0, 2)), "floor": 2, "cpu_used": 0, "cpu_cap": 0,
+        "needed": int(rng.integers(1, 150 * n)) * 1024,
+    }
+
+
+def test_k5_every_tree_size_across_the_shared_memory_limits(eng):
+    """Random trees of every size class around the single-CTA launch configurations
+    (zero-copy staging ~48 KB, block-size steps, the 4096-node limit) against the CPU
+    restatement (itself pinned to the reference's 402 golden vectors).  Regression: a 488-node
+    tree needed 48,888 B of dynamic + static shared memory, just over the 48 KB default."""
+    from oracle_ffi import oracle_evict
+    rng = np.random.default_rng(2024)
+    sizes = list(range(380, 620, 7)) + [63, 64, 65, 127, 128, 129, 1023, 1024, 1025, 1170, 1171, 2047, 2049, 4095,
+                                        4096, 4097]
+    checked = 0
+    for n in sizes:
+        for _ in range(8):  # skip snapshots that hit the reference's remove_node defect (rc 13)
+            c = random_case(rng, n)
+            rc, want, imm, pend = oracle_evict(c)
+            if rc == 0:
+                break
+        if rc != 0:
+            continue
+        ta = TreeArrays(c)
+        tree = {k: getattr(ta, k) for k in ("parent", "status", "lock", "rank", "time", "seq", "id", "tokens", "backed")}
+        tree["depth"] = depth_from_parent(ta.parent)
+        tree["bpt"] = ta.bpt
+        idx, act, gi, gp = eng.victims(tree, c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"],
+                                       c["cpu_used"], c["cpu_cap"])
+        got = [(int(ta.id[v]), int(ta.tokens[v]) * ta.bpt, 0 if a == 0 else 1) for v, a in zip(idx, act)]
+        assert got == want and (gi, gp) == (imm, pend), n
+        checked += 1
+    assert checked >= len(sizes) - 4

@@ -85,3 +85,19 @@ def test_c4_full_matches_reference():
     host = res_rec["offloaded_bytes"] // 131072 + 4096
     res, _ = run_against("sim_c4.jsonl", host_slots=host)
     assert res["prefetch_jobs"] == 157 and res["reactive_jobs"] == 336 and res["offload_jobs"] == 1261
+
+
+def test_c4_write_back_batching_keeps_decisions_and_bytes():
+    """§8f-4: write-backs leave as one K2 launch per evict call (the default); the unbatched
+    run (one launch per node) gives the identical trace and bytes.  Measured finding: C4's
+    make_room evicts exactly one node per call, so its 1,261 write-backs are 1,261 batches --
+    batching saves launches only when one call displaces several nodes."""
+    golden = load_jsonl("sim_c4_g8.jsonl")
+    res_rec = [r for r in golden if r["t"] == "res"][0]
+    host = res_rec["offloaded_bytes"] // 16384 + 4096
+    geom = dict(layers=32, kv_heads_total=8, kv_heads_local=1, head_offset=7, head_dim=128, host_slots=host)
+    batched, _ = run_against("sim_c4_g8.jsonl", **geom)
+    unbatched, _ = run_against("sim_c4_g8.jsonl", d2h_unbatched=1, **geom)
+    assert unbatched["d2h_batches"] == 0
+    assert 0 < batched["d2h_batches"] <= batched["offload_jobs"] == unbatched["offload_jobs"]
+    assert batched["kernel_launches"] <= unbatched["kernel_launches"]
