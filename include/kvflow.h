@@ -13,6 +13,7 @@
  *                            (the TransferDone event, scheduler.cpp:94-97)
  *   kvf_priority_propagate<- RadixCache::set_agent_priorities proj/src/radix_cache.cpp:266-285 [K4]
  *   kvf_victim_select     <- RadixCache::evict (selection) proj/src/radix_cache.cpp:302-372 [K5]
+ *   kvf_decode_attend     <- (new) decode-side consumer of the slot-run table, SURVEY §8f-3 [K6]
  *   kvf_slots_alloc/free  <- (new) token-slot pools; the reference keeps only a byte ledger
  *                            (GpuPool, proj/include/kvsim/tier_manager.hpp:38-46)
  *
@@ -211,6 +212,24 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
 int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_request* req, int32_t* out_idx,
                       uint8_t* out_action, uint32_t* out_count, uint64_t* out_immediate, uint64_t* out_pending);
 
+/* ---- decode-side consumer of the slot-run table ------------------------ */
+/* K6: one decode step of GQA attention, reading layer `layer`'s K and V IN PLACE from the
+ * HBM pool through each sequence's slot-run list (what RadixCache::match_prefix hands out,
+ * proj/src/radix_cache.cpp:88-140, plus the request's suffix) -- no compaction copy.
+ *   q, out:  device bf16 [batch][kv_heads_local * group][128]  (head_dim must be 128)
+ *   runs:    the sequences' run lists concatenated, run_counts[b] runs for sequence b (token
+ *            order); a sequence with no runs gets out = 0.
+ *   out[b][h] = softmax(scale * q[b][h] . K_b^T) V_b  over kv head h / group, fp32 softmax,
+ *            P rounded to bf16 before P.V (flash-decoding).
+ *   chunk_tokens: tokens per work item (multiple of 64 in [64, 1024]; 0 = sized to the SMs).
+ * Async on the engine's compute stream as job `job_id` (kvf_job_wait / elapsed / release);
+ * ordered after the engine's own payload writes.  A caller consuming a prefetched node
+ * fences first with kvf_compute_wait_job(prefetch job); q must be ready and out unused
+ * until the job completes. */
+int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
+                      const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale, void* out,
+                      uint32_t chunk_tokens);
+
 /* ---- payload (prefill emulation) and verification ----------------------------------- */
 /* Writes the deterministic payload of tokens with content ids cids[0..ntok) into the runs
  * (emulates prefill writing KV).  Async on the engine's compute stream. */
@@ -234,6 +253,7 @@ typedef struct {
     double k5_phase_ns[5];     /* K5 in-kernel phases: stage, sort, walks, victim sort, scan+out */
     double k5_phase_cycles[5]; /* the same phases in SM cycles (clock64)                       */
     uint64_t stale_errors;     /* non-sticky CUDA errors found pending at API entry (cleared) */
+    uint64_t attend_calls, attend_bytes; /* K6 calls, KV bytes they read */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

@@ -62,7 +62,8 @@ class Stats(C.Structure):
                 ("dev_bytes", C.c_uint64), ("h2d_jobs", C.c_uint64), ("d2h_jobs", C.c_uint64),
                 ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
                 ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5),
-                ("k5_phase_cycles", C.c_double * 5), ("stale_errors", C.c_uint64)]
+                ("k5_phase_cycles", C.c_double * 5), ("stale_errors", C.c_uint64), ("attend_calls", C.c_uint64),
+                ("attend_bytes", C.c_uint64)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature
@@ -105,6 +106,8 @@ _ENGINE_SIGS = {
     "kvf_victim_select": (C.c_int, [C.c_void_p, C.POINTER(TreeView), C.POINTER(EvictRequest), C.c_void_p,
                                     C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint64),
                                     C.POINTER(C.c_uint64)]),
+    "kvf_decode_attend": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                    C.POINTER(Run), C.c_void_p, C.c_float, C.c_void_p, C.c_uint32]),
     "kvf_fill_payload": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_checksum": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.POINTER(C.c_uint64)]),
     "kvf_payload_checksum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),

@@ -187,6 +187,23 @@ void recycle_event(kvf_engine* e, cudaEvent_t ev) {
     if (ev) e->event_pool.push_back(ev);
 }
 
+int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j) {
+    if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
+    int rc = acquire_event(e, &j.start);
+    if (rc) return rc;
+    rc = acquire_event(e, &j.stop);
+    if (rc) return rc;
+    j.stream = stream;
+    KVF_CUDA(cudaEventRecord(j.start, stream));
+    return KVF_OK;
+}
+
+int end_job(kvf_engine* e, uint64_t job_id, Job& j) {
+    KVF_CUDA(cudaEventRecord(j.stop, j.stream));
+    e->jobs.emplace(job_id, j);
+    return KVF_OK;
+}
+
 }  // namespace kvf_impl
 
 // =====================================================================================
@@ -579,23 +596,6 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
     return KVF_OK;
 }
 
-int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j) {
-    if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
-    int rc = acquire_event(e, &j.start);
-    if (rc) return rc;
-    rc = acquire_event(e, &j.stop);
-    if (rc) return rc;
-    j.stream = stream;
-    KVF_CUDA(cudaEventRecord(j.start, stream));
-    return KVF_OK;
-}
-
-int end_job(kvf_engine* e, uint64_t job_id, Job& j) {
-    KVF_CUDA(cudaEventRecord(j.stop, j.stream));
-    e->jobs.emplace(job_id, j);
-    return KVF_OK;
-}
-
 int transfer(kvf_engine* e, uint64_t job_id, int src_tier, const kvf_run* src_runs, uint32_t n_src, int dst_tier,
              const kvf_run* dst_runs, uint32_t n_dst) {
     uint64_t ts = 0, td = 0;
@@ -796,7 +796,8 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
         (err = cudaStreamCreateWithPriority(&e->s_dec, cudaStreamNonBlocking, hi)) != cudaSuccess)
         return fail(cuda_error(err, "cudaStreamCreate"));
     if ((err = cudaEventCreateWithFlags(&e->dev_write_done, cudaEventDisableTiming)) != cudaSuccess ||
-        (err = cudaEventCreate(&e->dec_start)) != cudaSuccess || (err = cudaEventCreate(&e->dec_stop)) != cudaSuccess)
+        (err = cudaEventCreate(&e->dec_start)) != cudaSuccess || (err = cudaEventCreate(&e->dec_stop)) != cudaSuccess ||
+        (err = cudaEventCreateWithFlags(&e->att_upload_done, cudaEventDisableTiming)) != cudaSuccess)
         return fail(cuda_error(err, "cudaEventCreate"));
     if ((err = cudaMalloc(reinterpret_cast<void**>(&e->d_checksum), sizeof(uint64_t))) != cudaSuccess)
         return fail(cuda_error(err, "cudaMalloc(checksum)"));
@@ -823,12 +824,13 @@ int kvf_engine_destroy(kvf_engine* e) {
         cudaEventDestroy(j.stop);
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : {e->dev_write_done, e->dec_start, e->dec_stop})
+    for (cudaEvent_t ev : {e->dev_write_done, e->dec_start, e->dec_stop, e->att_upload_done})
         if (ev) cudaEventDestroy(ev);
     for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp})
         if (s) cudaStreamDestroy(s);
     e->ws_dev.release();
     e->ws_dec.release();
+    e->ws_att.release();
     for (auto& kv : e->big_graphs) cudaGraphExecDestroy(kv.second.exec);
     e->ws_big.release();
     if (e->d_checksum) cudaFree(e->d_checksum);

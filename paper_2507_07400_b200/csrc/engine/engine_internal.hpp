@@ -112,6 +112,9 @@ struct kvf_engine {
 
     kvf_impl::Workspace ws_dev;  // fill / checksum / read staging (s_dev)
     kvf_impl::Workspace ws_dec;  // decision kernels (s_dec)
+    kvf_impl::Workspace ws_att;  // K6 decode attention: descriptors + partials (s_cmp)
+    cudaEvent_t att_upload_done = nullptr;  // last K6 descriptor upload out of ws_att.host
+    bool att_upload_pending = false, attend_attr_set = false;
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
     std::map<uint64_t, kvf_impl::BigGraph> big_graphs;  // key: bucket << 1 | workflow_aware
 
@@ -126,6 +129,9 @@ struct kvf_engine {
 
 namespace kvf_impl {
 int acquire_event(kvf_engine* e, cudaEvent_t* ev);
+// a job = start event on `stream` ... kernels ... stop event (end_job registers it)
+int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j);
+int end_job(kvf_engine* e, uint64_t job_id, Job& j);
 void clear_stale_error(kvf_engine* e, const char* fn);
 int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
                         uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend);

@@ -163,6 +163,16 @@ class Engine:
         N.check(self._lib.kvf_dev_scatter(self.h, job, staging_ptr, N.runs_array(dev_runs), len(dev_runs)))
         return job
 
+    def attend(self, layer, group, q_ptr, seq_runs, out_ptr, scale, job=None, chunk=0):
+        """K6: decode attention of layer `layer` over each sequence's slot runs, in place
+        (q/out: device bf16 [batch][kv_heads_local*group][128]).  Async job on the compute stream."""
+        job = job or self.new_job()
+        flat = [r for runs in seq_runs for r in runs]
+        counts = np.array([len(r) for r in seq_runs], dtype=np.uint32)
+        N.check(self._lib.kvf_decode_attend(self.h, job, layer, len(seq_runs), group, q_ptr, N.runs_array(flat),
+                                            counts.ctypes.data, float(scale), out_ptr, chunk))
+        return job
+
     def query(self, job):
         d = C.c_int32()
         N.check(self._lib.kvf_job_query(self.h, job, C.byref(d)))

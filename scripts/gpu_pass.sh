@@ -1,0 +1,11 @@
+# One GPU call: full pass (smoke, -m gpu, bench both arms, crossover) + launch list + ncu captures.
+tag=${1:-r01}
+mkdir -p gpurun_out
+nvidia-smi topo -m > gpurun_out/topo_$tag.txt 2>&1; nproc > gpurun_out/nproc_$tag.txt; lscpu >> gpurun_out/nproc_$tag.txt
+bash scripts/gpu_full.sh $tag
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 3 --warmup 3 > gpurun_out/bench_under_ncu_$tag.log 2>&1; tail -2 gpurun_out/bench_under_ncu_$tag.log
+for k in k1 k3 k5; do
+  pat=kvf_copy_vec; [ $k = k5 ] && pat=kvf_victim
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$pat -s 2 -c 1 -o gpurun_out/prof_${k}_$tag python scripts/profile_kernels.py $k > gpurun_out/ncu_${k}_$tag.log 2>&1; tail -3 gpurun_out/ncu_${k}_$tag.log
+done
+ls -la gpurun_out

@@ -1,0 +1,190 @@
+"""K6 kvf_decode_attend -- the decode-side consumer of the slot-run table.
+
+Floating point, so the oracle here is a plain PyTorch fp32 restatement of decode attention
+(softmax(scale * q K^T) V per KV-head group) over the LOGICAL token order of each sequence,
+computed from the same bf16 K/V the test wrote.  The kernel reads the same bytes through
+fragmented slot runs (ragged lengths, shared prefixes, > 64 runs per work item, empty
+sequences).  Tolerance (written here, from the kernel's numerics): P is rounded to bf16
+before P.V and the output is bf16, so |out - ref| <= 1.5e-2 + 1.5e-2 |ref| per element and
+the mean abs error <= 2e-3.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+N = pytest.importorskip("paper_2507_07400_b200._native")
+from paper_2507_07400_b200.engine import Engine  # noqa: E402
+
+ATOL = RTOL = 1.5e-2
+MEAN_TOL = 2e-3
+
+
+def need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def write_runs(e, runs, planes_tokens):
+    """Write logical KV [planes][ntok][H][128] (bf16, cuda) into the runs via K3 scatter."""
+    st = planes_tokens.contiguous()
+    torch.cuda.synchronize()
+    j = e.dev_scatter(st.data_ptr(), runs)
+    e.wait(j)
+    e.release(j)
+
+
+def fragmented_runs(e, ntok, rng, max_piece):
+    """ntok slots as many short runs (alloc small blocks, free every other one first)."""
+    runs, left = [], ntok
+    while left:
+        n = int(min(left, rng.integers(1, max_piece + 1)))
+        got = e.alloc(N.KVF_TIER_DEVICE, n)
+        runs += got
+        pad = e.alloc(N.KVF_TIER_DEVICE, int(rng.integers(1, 4)))  # a hole so runs never merge
+        e.free(N.KVF_TIER_DEVICE, pad)
+        left -= n
+    return runs
+
+
+def reference(q, kv_list, layer, group, scale):
+    """fp32 decode attention; q [B][Hq][128] bf16, kv_list[b] = [planes][n_b][H][128]."""
+    outs = []
+    for b, kv in enumerate(kv_list):
+        hq = q.shape[1]
+        if kv is None or kv.shape[1] == 0:
+            outs.append(torch.zeros(hq, 128, device=q.device))
+            continue
+        k = kv[2 * layer].float()          # [n][H][D]
+        v = kv[2 * layer + 1].float()
+        qq = q[b].float().view(k.shape[1], group, 128)  # [H][G][D]
+        s = torch.einsum("hgd,nhd->hgn", qq, k) * scale
+        p = torch.softmax(s, dim=-1)
+        outs.append(torch.einsum("hgn,nhd->hgd", p, v).reshape(hq, 128))
+    return torch.stack(outs)
+
+
+def check(out, ref):
+    o = out.float()
+    err = (o - ref).abs()
+    assert torch.isfinite(o).all()
+    bad = err > ATOL + RTOL * ref.abs()
+    assert not bad.any(), f"max err {err.max().item():.4g} at {bad.nonzero()[:4].tolist()}"
+    assert err.mean().item() <= MEAN_TOL, err.mean().item()
+
+
+@pytest.mark.parametrize("kv_local,group,chunk", [(8, 4, 0), (8, 4, 64), (8, 4, 1024), (2, 8, 0), (1, 8, 128),
+                                                  (8, 1, 256), (4, 16, 0)])
+def test_attend_ragged_fragmented(kv_local, group, chunk):
+    need_gpu()
+    rng = np.random.default_rng(kv_local * 100 + group + chunk)
+    torch.manual_seed(kv_local * 7 + group)
+    layers = 3
+    lens = [1, 15, 16, 64, 100, 1000, 4097, 0, 300]
+    with Engine(layers=layers, kv_heads_total=8, kv_heads_local=kv_local, head_offset=8 - kv_local,
+                gpu_slots=sum(lens) * 2 + 4096, host_slots=0) as e:
+        seq_runs, kvs = [], []
+        for i, n in enumerate(lens):
+            if n == 0:
+                seq_runs.append([])
+                kvs.append(None)
+                continue
+            runs = fragmented_runs(e, n, rng, max_piece=[7, 50, 700][i % 3])
+            kv = torch.randn(2 * layers, n, kv_local, 128, device="cuda").to(torch.bfloat16)
+            write_runs(e, runs, kv)
+            seq_runs.append(runs)
+            kvs.append(kv)
+        B, hq = len(lens), kv_local * group
+        q = torch.randn(B, hq, 128, device="cuda").to(torch.bfloat16)
+        out = torch.full((B, hq, 128), float("nan"), device="cuda", dtype=torch.bfloat16)
+        scale = 1.0 / math.sqrt(128)
+        for layer in range(layers):
+            torch.cuda.synchronize()
+            j = e.attend(layer, group, q.data_ptr(), seq_runs, out.data_ptr(), scale, chunk=chunk)
+            e.wait(j)
+            e.release(j)
+            check(out, reference(q, kvs, layer, group, scale))
+
+
+def test_attend_shared_prefix_and_many_runs():
+    """Two requests sharing a radix prefix (same slots) + own suffixes; one sequence of 300
+    runs of 3 tokens (work items cut at 64 runs)."""
+    need_gpu()
+    rng = np.random.default_rng(5)
+    with Engine(layers=1, kv_heads_total=8, gpu_slots=40000, host_slots=0) as e:
+        prefix = fragmented_runs(e, 2000, rng, 300)
+        pkv = torch.randn(2, 2000, 8, 128, device="cuda").to(torch.bfloat16)
+        write_runs(e, prefix, pkv)
+        seqs, kvs = [], []
+        for n in (1, 77, 600):
+            suf = e.alloc(N.KVF_TIER_DEVICE, n)
+            skv = torch.randn(2, n, 8, 128, device="cuda").to(torch.bfloat16)
+            write_runs(e, suf, skv)
+            seqs.append(prefix + suf)
+            kvs.append(torch.cat([pkv, skv], dim=1))
+        many = []
+        for _ in range(300):
+            many += e.alloc(N.KVF_TIER_DEVICE, 3)
+            e.free(N.KVF_TIER_DEVICE, e.alloc(N.KVF_TIER_DEVICE, 1))
+        mkv = torch.randn(2, 900, 8, 128, device="cuda").to(torch.bfloat16)
+        write_runs(e, many, mkv)
+        assert len(many) >= 200
+        seqs.append(many)
+        kvs.append(mkv)
+        q = torch.randn(len(seqs), 32, 128, device="cuda").to(torch.bfloat16)
+        out = torch.empty(len(seqs), 32, 128, device="cuda", dtype=torch.bfloat16)
+        for chunk in (0, 64, 512):
+            torch.cuda.synchronize()
+            j = e.attend(0, 4, q.data_ptr(), seqs, out.data_ptr(), 0.088, chunk=chunk)
+            e.wait(j)
+            e.release(j)
+            check(out, reference(q, kvs, 0, 4, 0.088))
+
+
+def test_attend_consumes_prefetched_node_in_place():
+    """K1 prefetch of a host node into fragmented HBM runs, the compute stream fenced on the
+    prefetch job (kvf_compute_wait_job), then K6 straight on the prefetched runs."""
+    need_gpu()
+    rng = np.random.default_rng(9)
+    n = 3000
+    with Engine(layers=2, kv_heads_total=8, gpu_slots=8192, host_slots=4096) as e:
+        host = e.alloc(N.KVF_TIER_HOST, n)
+        kv = torch.randn(4, n, 8, 128).to(torch.bfloat16)
+        # host pool layout [plane][slot][head][dim]: write the node's tokens into its slots
+        pool = e.host_pool_array().view(np.uint16).reshape(4, e.host_slots, 8, 128)
+        t = 0
+        for s, l in host:
+            pool[:, s:s + l] = kv[:, t:t + l].view(torch.int16).numpy().view(np.uint16)
+            t += l
+        dev = fragmented_runs(e, n, rng, 400)
+        jp = e.h2d(host, dev)              # K1 on the H2D stream
+        e.compute_wait_job(jp)             # the consumer's fence, on the GPU
+        q = torch.randn(1, 32, 128, device="cuda").to(torch.bfloat16)
+        out = torch.empty(1, 32, 128, device="cuda", dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        ja = e.attend(1, 4, q.data_ptr(), [dev], out.data_ptr(), 0.1)
+        e.wait(ja)
+        e.release(ja)
+        e.release(jp)
+        check(out, reference(q, [kv.cuda()], 1, 4, 0.1))
+
+
+def test_attend_errors():
+    need_gpu()
+    with Engine(layers=1, kv_heads_total=8, gpu_slots=256, host_slots=0) as e:
+        q = torch.zeros(1, 32, 128, device="cuda", dtype=torch.bfloat16)
+        out = torch.zeros_like(q)
+        with pytest.raises(N.KvfError):
+            e.attend(1, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)    # layer out of range
+        with pytest.raises(N.KvfError):
+            e.attend(0, 4, q.data_ptr(), [[(250, 10)]], out.data_ptr(), 1.0)  # run beyond the pool
+        with pytest.raises(N.KvfError):
+            e.attend(0, 17, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)   # group > 16
+        with pytest.raises(N.KvfError):
+            e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0, chunk=100)
+    with Engine(layers=1, kv_heads_total=8, head_dim=64, gpu_slots=256, host_slots=0) as e:
+        with pytest.raises(N.KvfError):
+            e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)    # head_dim 128 only
