@@ -221,7 +221,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_
  *            order); a sequence with no runs gets out = 0.
  *   out[b][h] = softmax(scale * q[b][h] . K_b^T) V_b  over kv head h / group, fp32 softmax,
  *            P rounded to bf16 before P.V (flash-decoding).
- *   chunk_tokens: tokens per work item (multiple of 64 in [64, 1024]; 0 = sized to the SMs).
+ *   chunk_tokens: tokens per work item (multiple of 16 in [16, 2048]; 0 = one wave of CTAs).
  * Async on the engine's compute stream as job `job_id` (kvf_job_wait / elapsed / release);
  * ordered after the engine's own payload writes.  A caller consuming a prefetched node
  * fences first with kvf_compute_wait_job(prefetch job); q must be ready and out unused

@@ -10,23 +10,32 @@
 // does 4 flop per KV byte: HBM-bound by ~50x on the tensor cores.  tcgen05 needs M >= 64
 // rows and only G of them would be live, so the kernel uses the warp-level HMMA path
 // (mma.sync m16n8k16 bf16 -> fp32) whose 16-row tile wastes less, and spends its design
-// on the bytes: every (token, head) row of K and V is a 256-B line fetched once with
-// 16-B cp.async (LDGSTS) straight into a 128-B-XOR-swizzled shared-memory tile (so the
-// ldmatrix reads are conflict-free), three 64-token stages in flight per CTA, two CTAs
-// per SM.  The slot of every token is resolved once per CTA from the run table
-// (binary search in shared memory), which is what makes arbitrary split points
-// (radix_cache.cpp:142-177) free for the consumer too.
-//
-// Work split (flash-decoding): a work item = (sequence, <= chunk tokens, <= kMaxRuns runs);
-// grid = items x local KV heads.  Each CTA keeps an online softmax per warp, merges its 4
-// warps in shared memory and writes an unnormalised partial (m, l, o[G][128]); a second
-// kernel merges a sequence's partials per query head.
+// on the bytes:
+//  * one CTA (8 warps, one per SM) covers ALL local KV heads of a token range, so the
+//    rows it has in flight are whole contiguous token rows of the pool (2 KiB per token
+//    per plane for 8 heads) -- DRAM pages are read densely, not in scattered 256-B pieces;
+//  * every (token, head) row of K and V is fetched once with 16-B cp.async (LDGSTS, L1
+//    bypass) straight into an XOR-swizzled shared-memory tile, so ldmatrix is
+//    bank-conflict free; each warp streams its own 16-token tiles through a private
+//    3-stage ring (no CTA barrier in the loop): 8 warps x 2-3 tiles x 8 KiB in flight;
+//  * work is sized to ONE wave of CTAs: a decode layer is ~20 us of HBM time, so a second
+//    partial wave costs as much as the layer;
+//  * the slot of every token is resolved once per CTA from the run table (binary search
+//    in shared memory) -- arbitrary radix split points (radix_cache.cpp:142-177) are free
+//    for the consumer too;
+//  * flash-decoding split: a sequence cut into k > 1 work items writes k unnormalised
+//    partials (m, l, o) and a combine kernel, launched with programmatic dependent launch
+//    so its launch overlaps the main kernel's tail, merges them; k = 1 writes out directly.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <numeric>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -36,21 +45,26 @@ using namespace kvf_impl;
 
 namespace {
 
-constexpr int kD = 128;                     // head_dim (Llama-3 8B / 70B)
-constexpr int kWarps = 4;
+constexpr int kD = 128;                       // head_dim (Llama-3 8B / 70B)
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int kTokWarp = 16;                // tokens per warp per stage (one m16n8k16 K step)
-constexpr int kStageTok = kWarps * kTokWarp;  // 64
-constexpr int kStages = 3;
-constexpr int kRowBytes = kD * 2;           // one (token, head) row of K or V: 256 B
-constexpr int kStageBytes = kStageTok * kRowBytes * 2;  // K + V: 32 KiB
-constexpr int kMaxRuns = 64;                // runs one work item may span
-constexpr int kMaxChunk = 1024;             // tokens per work item
-constexpr int kMaxGroup = 16;               // q heads per kv head (m16 tile rows)
-constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + kMaxChunk * 4 + kMaxRuns * 8;
+constexpr int kTok = 16;                      // tokens per tile (one m16n8k16 K step of P.V)
+constexpr int kRowBytes = kD * 2;             // one (token, head) row of K or V: 256 B
+constexpr int kTileBytes = kTok * kRowBytes;  // 4 KiB of K (and 4 KiB of V)
+constexpr int kStages = 3;                    // per-warp ring depth
+constexpr int kWarpRing = kStages * 2 * kTileBytes;  // 24 KiB
+constexpr int kMaxRuns = 64;                  // runs one work item may span
+constexpr int kMaxChunk = 2048;               // tokens per work item
+constexpr int kMaxGroup = 16;                 // q heads per kv head (m16 tile rows)
+constexpr int kMaxHeadsCta = 8;               // KV heads one CTA covers
+constexpr size_t kSmemBytes = static_cast<size_t>(kWarps) * kWarpRing + kMaxChunk * 4 + kMaxRuns * 8;
+constexpr int kRedStride = kD + 8;            // floats per row of the warp-merge buffer
+static_assert(kWarps * kWarpRing >= kWarps * 16 * kRedStride * 4 + 2 * kWarps * 16 * 4, "merge buffers reuse the rings");
 
 struct AttnItem {
-    uint32_t seq, t0, ntok, r0, nr, pad0, pad1, pad2;  // 32 B
+    uint32_t seq, t0, ntok, r0, nr;
+    uint32_t nsib;  // items of this sequence (1: the CTA writes the output itself)
+    uint32_t pad0, pad1;  // 32 B
 };
 
 struct AttnParams {
@@ -59,19 +73,27 @@ struct AttnParams {
     uint32_t tpb;            // bytes per token per plane (kv_heads_local * 256)
     uint32_t layer;
     uint32_t group, hq;      // q heads per kv head, q heads per sequence (local)
+    uint32_t hkv, hpc;       // local kv heads, kv heads per CTA (divides 8 and hkv)
     float scale_log2;        // softmax scale * log2(e)
     const __nv_bfloat16* q;  // [batch][hq][128]
+    __nv_bfloat16* out;      // [batch][hq][128]
     const AttnItem* items;
     const uint32_t* run_tok;   // token offset of each run within its sequence
     const uint32_t* run_slot;  // first slot of each run
-    float* part_o;             // [items][kv_heads_local][group][128]
-    float* part_ml;            // [items][kv_heads_local][group][2]
+    float* part_o;             // [items][hkv][group][128]
+    float* part_ml;            // [items][hkv][group][2]
+    unsigned long long* trace; // diagnostics (KVF_ATTEND_TRACE): per CTA start, prologue, loop, end, smid
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
     const int n = valid ? 16 : 0;  // zero-fill rows past the item's tokens
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(n));
@@ -101,21 +123,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
 }
-// byte offset of 16-B chunk c of row r inside a [rows][256 B] tile (XOR swizzle on the low 3 bits)
+// byte offset of 16-B chunk c of row r inside a [16 rows][256 B] tile (XOR swizzle, low 3 bits)
 __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return r * kRowBytes + ((c ^ (r & 7)) << 4); }
 
-__global__ void __launch_bounds__(kThreads, 2) kvf_attend_kernel(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_constant__ AttnParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* stage_base = smem;
-    uint32_t* slot_s = reinterpret_cast<uint32_t*>(smem + kStages * kStageBytes);
+    uint32_t* slot_s = reinterpret_cast<uint32_t*>(smem + kWarps * kWarpRing);
     uint32_t* rtok_s = slot_s + kMaxChunk;
     uint32_t* rslot_s = rtok_s + kMaxRuns;
 
-    const AttnItem it = p.items[blockIdx.x];
-    const uint32_t head = blockIdx.y;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long t_start = p.trace ? gtime() : 0;
+    const AttnItem it = p.items[blockIdx.x];
+    // warp -> (head, sub-stream): the CTA's hpc heads x (8 / hpc) interleaved tile streams
+    const uint32_t hl = warp % p.hpc, sub = warp / p.hpc, nsub = kWarps / p.hpc;
+    const uint32_t head = blockIdx.y * p.hpc + hl;
 
-    // ---- resolve the item's token -> slot map once (runs cached in smem, binary search)
+    // ---- Q fragments (A operand: rows = the group's q heads, zero beyond G); issued first,
+    // they land while the slot map is being resolved
+    const uint32_t g = lane >> 2, cq = 2 * (lane & 3);
+    const __nv_bfloat16* qb = p.q + (static_cast<uint64_t>(it.seq) * p.hq + head * p.group) * kD;
+    uint32_t qa[8][4];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t d0 = kk * 16 + cq;
+        qa[kk][0] = g < p.group ? *reinterpret_cast<const uint32_t*>(qb + g * kD + d0) : 0u;
+        qa[kk][1] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * kD + d0) : 0u;
+        qa[kk][2] = g < p.group ? *reinterpret_cast<const uint32_t*>(qb + g * kD + d0 + 8) : 0u;
+        qa[kk][3] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * kD + d0 + 8) : 0u;
+    }
+
+    // ---- token -> slot map of the item (runs cached in smem, one binary search per token)
     for (uint32_t r = tid; r < it.nr; r += kThreads) {
         rtok_s[r] = p.run_tok[it.r0 + r];
         rslot_s[r] = p.run_slot[it.r0 + r];
@@ -132,36 +170,28 @@ __global__ void __launch_bounds__(kThreads, 2) kvf_attend_kernel(const __grid_co
     }
     __syncthreads();
 
+    const unsigned long long t_pro = p.trace ? gtime() : 0;
+    // ---- per-warp pipeline over tiles sub, sub + nsub, ... of the item, for its head
     const char* kplane = p.pool + static_cast<uint64_t>(2 * p.layer) * p.plane_stride + head * kRowBytes;
     const char* vplane = kplane + p.plane_stride;
-    const uint32_t nst = (it.ntok + kStageTok - 1) / kStageTok;
-    const uint32_t lc = tid & 15, lr = tid >> 4;  // this thread's 16-B column, first row (8 rows apart)
+    uint8_t* ring = smem + warp * kWarpRing;
+    const uint32_t ntiles = (it.ntok + kTok - 1) / kTok;
+    const uint32_t mine = sub < ntiles ? (ntiles - sub + nsub - 1) / nsub : 0;
+    const uint32_t lc = lane & 15, lr = lane >> 4;  // 16-B column; rows lr, lr+2, ..., lr+14
 
-    auto issue = [&](uint32_t s) {
-        uint8_t* kb = stage_base + (s % kStages) * kStageBytes;
-        uint8_t* vb = kb + kStageTok * kRowBytes;
+    auto issue = [&](uint32_t i) {
+        uint8_t* kb = ring + (i % kStages) * 2 * kTileBytes;
+        uint8_t* vb = kb + kTileBytes;
+        const uint32_t tb = (sub + i * nsub) * kTok;
 #pragma unroll
-        for (int i = 0; i < kStageTok / 8; ++i) {
-            const uint32_t r = lr + 8 * i, j = s * kStageTok + r;
+        for (int k = 0; k < kTok / 2; ++k) {
+            const uint32_t r = lr + 2 * k, j = tb + r;
             const bool ok = j < it.ntok;
-            const uint64_t off = static_cast<uint64_t>(ok ? slot_s[j] : slot_s[0]) * p.tpb + lc * 16;
+            const uint64_t off = static_cast<uint64_t>(slot_s[ok ? j : 0]) * p.tpb + lc * 16;
             cp_async16(smem_u32(kb + swz(r, lc)), kplane + off, ok);
             cp_async16(smem_u32(vb + swz(r, lc)), vplane + off, ok);
         }
     };
-
-    // ---- Q fragments (A operand, rows = the group's q heads, zero beyond G), loaded once
-    const uint32_t g = lane >> 2, cq = 2 * (lane & 3);
-    const __nv_bfloat16* qb = p.q + (static_cast<uint64_t>(it.seq) * p.hq + head * p.group) * kD;
-    uint32_t qa[8][4];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t d0 = kk * 16 + cq;
-        qa[kk][0] = g < p.group ? *reinterpret_cast<const uint32_t*>(qb + g * kD + d0) : 0u;
-        qa[kk][1] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * kD + d0) : 0u;
-        qa[kk][2] = g < p.group ? *reinterpret_cast<const uint32_t*>(qb + g * kD + d0 + 8) : 0u;
-        qa[kk][3] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * kD + d0 + 8) : 0u;
-    }
 
     float acc[16][4];
 #pragma unroll
@@ -169,92 +199,103 @@ __global__ void __launch_bounds__(kThreads, 2) kvf_attend_kernel(const __grid_co
     float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows g and g+8
 
 #pragma unroll
-    for (uint32_t s = 0; s < kStages - 1; ++s) {
-        if (s < nst) issue(s);
+    for (uint32_t i = 0; i < kStages - 1; ++i) {
+        if (i < mine) issue(i);
         cp_async_commit();
     }
-    for (uint32_t s = 0; s < nst; ++s) {
-        if (s + kStages - 1 < nst) issue(s + kStages - 1);
+    const uint32_t krow = (lane & 7) + ((lane >> 4) << 3), kcol = (lane >> 3) & 1;
+    const uint32_t vrow = (lane & 7) + (((lane >> 3) & 1) << 3), vcol = lane >> 4;
+    for (uint32_t i = 0; i < mine; ++i) {
+        if (i + kStages - 1 < mine) issue(i + kStages - 1);
         cp_async_commit();
         cp_async_wait<kStages - 1>();
-        __syncthreads();
-        const uint32_t tbase = s * kStageTok + warp * kTokWarp;  // first token of this warp's slice
-        if (tbase < it.ntok) {
-            const uint8_t* kb = stage_base + (s % kStages) * kStageBytes;
-            const uint8_t* vb = kb + kStageTok * kRowBytes;
-            const uint32_t row0 = warp * kTokWarp;
-            // S^T tile: 16 q rows x 16 tokens (two n8 tiles), K = 128 dims
-            float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint32_t krow = row0 + (lane & 7) + ((lane >> 4) << 3), kcol = (lane >> 3) & 1;
+        __syncwarp();
+        const uint8_t* kb = ring + (i % kStages) * 2 * kTileBytes;
+        const uint8_t* vb = kb + kTileBytes;
+        const uint32_t tb = (sub + i * nsub) * kTok;
+        // S^T tile: 16 q rows x 16 tokens (two n8 tiles), K = 128 dims
+        float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(smem_u32(kb + swz(krow, 2 * kk + kcol)), b0, b1, b2, b3);
-                mma16816(s0, qa[kk], b0, b1);
-                mma16816(s1, qa[kk], b2, b3);
-            }
-            // online softmax over this 16-token slice (masked tokens -> -inf)
-            const uint32_t tA = tbase + cq, tB = tbase + 8 + cq;
-            float x[8] = {s0[0], s0[1], s0[2], s0[3], s1[0], s1[1], s1[2], s1[3]};
-            const bool v[8] = {tA < it.ntok, tA + 1 < it.ntok, tA < it.ntok, tA + 1 < it.ntok,
-                               tB < it.ntok, tB + 1 < it.ntok, tB < it.ntok, tB + 1 < it.ntok};
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = v[i] ? x[i] * p.scale_log2 : -INFINITY;
-            float mx0 = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[4], x[5]));
-            float mx1 = fmaxf(fmaxf(x[2], x[3]), fmaxf(x[6], x[7]));
-#pragma unroll
-            for (int o = 1; o <= 2; o <<= 1) {
-                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-            }
-            const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);  // finite: every slice has a valid token
-            const float a0 = exp2f(m0 - n0), a1 = exp2f(m1 - n1);
-            m0 = n0;
-            m1 = n1;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = exp2f(x[i] - ((i & 2) ? n1 : n0));
-            l0 = l0 * a0 + x[0] + x[1] + x[4] + x[5];
-            l1 = l1 * a1 + x[2] + x[3] + x[6] + x[7];
-#pragma unroll
-            for (int n = 0; n < 16; ++n) {
-                acc[n][0] *= a0;
-                acc[n][1] *= a0;
-                acc[n][2] *= a1;
-                acc[n][3] *= a1;
-            }
-            // P (bf16) as the A operand of P.V: the S accumulator layout maps onto it directly
-            const uint32_t pa[4] = {pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]),
-                                    pack_bf16(x[6], x[7])};
-            const uint32_t vrow = row0 + (lane & 7) + (((lane >> 3) & 1) << 3), vcol = lane >> 4;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(smem_u32(vb + swz(vrow, 2 * j + vcol)), b0, b1, b2, b3);
-                mma16816(acc[2 * j], pa, b0, b1);
-                mma16816(acc[2 * j + 1], pa, b2, b3);
-            }
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(smem_u32(kb + swz(krow, 2 * kk + kcol)), b0, b1, b2, b3);
+            mma16816(s0, qa[kk], b0, b1);
+            mma16816(s1, qa[kk], b2, b3);
         }
-        __syncthreads();  // the stage buffer is refilled next iteration
+        // online softmax over the tile (masked tokens -> -inf; token tb is always valid)
+        const uint32_t tA = tb + cq, tB = tb + 8 + cq;
+        float x[8] = {s0[0], s0[1], s0[2], s0[3], s1[0], s1[1], s1[2], s1[3]};
+        const bool v[8] = {tA < it.ntok, tA + 1 < it.ntok, tA < it.ntok, tA + 1 < it.ntok,
+                           tB < it.ntok, tB + 1 < it.ntok, tB < it.ntok, tB + 1 < it.ntok};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = v[k] ? x[k] * p.scale_log2 : -INFINITY;
+        float mx0 = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[4], x[5]));
+        float mx1 = fmaxf(fmaxf(x[2], x[3]), fmaxf(x[6], x[7]));
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        }
+        const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+        const float a0 = exp2f(m0 - n0), a1 = exp2f(m1 - n1);
+        m0 = n0;
+        m1 = n1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = exp2f(x[k] - ((k & 2) ? n1 : n0));
+        l0 = l0 * a0 + x[0] + x[1] + x[4] + x[5];
+        l1 = l1 * a1 + x[2] + x[3] + x[6] + x[7];
+#pragma unroll
+        for (int n = 0; n < 16; ++n) {
+            acc[n][0] *= a0;
+            acc[n][1] *= a0;
+            acc[n][2] *= a1;
+            acc[n][3] *= a1;
+        }
+        // P (bf16) as the A operand of P.V: the S accumulator layout maps onto it directly
+        const uint32_t pa[4] = {pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]),
+                                pack_bf16(x[6], x[7])};
+#pragma unroll
+        for (int jn = 0; jn < 8; ++jn) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(smem_u32(vb + swz(vrow, 2 * jn + vcol)), b0, b1, b2, b3);
+            mma16816(acc[2 * jn], pa, b0, b1);
+            mma16816(acc[2 * jn + 1], pa, b2, b3);
+        }
+        __syncwarp();  // this ring slot is refilled next iteration
     }
     cp_async_wait<0>();
-    __syncthreads();
+    if (p.trace) {
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long* tr = p.trace + (static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5;
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+            tr[0] = t_start;
+            tr[1] = t_pro;
+            tr[2] = gtime();
+            tr[4] = smid;
+        }
+    }
 
-    // ---- merge the 4 warps' partials in shared memory (reusing the stage buffers)
+    // ---- merge the warps of each head in shared memory (the rings are free once all are here)
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, o);
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
-    float* red_o = reinterpret_cast<float*>(stage_base);              // [warp][16 rows][128]
-    float* red_m = red_o + kWarps * 16 * kD;                           // [warp][16]
+    __syncthreads();
+    // [warp][16 rows][kRedStride]: the 8-float pad puts the 8 row groups of a float2 store in
+    // distinct banks (2 wavefronts per store instead of 8); rows >= group are never stored
+    float* red_o = reinterpret_cast<float*>(smem);
+    float* red_m = red_o + kWarps * 16 * kRedStride;  // [warp][16]
     float* red_l = red_m + kWarps * 16;
 #pragma unroll
     for (int n = 0; n < 16; ++n) {
         const uint32_t d = n * 8 + cq;
-        red_o[(warp * 16 + g) * kD + d] = acc[n][0];
-        red_o[(warp * 16 + g) * kD + d + 1] = acc[n][1];
-        red_o[(warp * 16 + g + 8) * kD + d] = acc[n][2];
-        red_o[(warp * 16 + g + 8) * kD + d + 1] = acc[n][3];
+        if (g < p.group)
+            *reinterpret_cast<float2*>(&red_o[(warp * 16 + g) * kRedStride + d]) = make_float2(acc[n][0], acc[n][1]);
+        if (g + 8 < p.group)
+            *reinterpret_cast<float2*>(&red_o[(warp * 16 + g + 8) * kRedStride + d]) = make_float2(acc[n][2], acc[n][3]);
     }
     if ((lane & 3) == 0) {
         red_m[warp * 16 + g] = m0;
@@ -263,46 +304,113 @@ __global__ void __launch_bounds__(kThreads, 2) kvf_attend_kernel(const __grid_co
         red_l[warp * 16 + g + 8] = l1;
     }
     __syncthreads();
-    const uint64_t pbase = static_cast<uint64_t>(blockIdx.x) * gridDim.y + head;
-    for (uint32_t e = tid; e < p.group * kD; e += kThreads) {
-        const uint32_t row = e / kD, d = e % kD;
+    // outputs of this CTA: hpc heads x group rows x 128 dims, 4 dims per thread step
+    for (uint32_t e = tid; e < p.hpc * p.group * (kD / 4); e += kThreads) {
+        const uint32_t h = e / (p.group * (kD / 4)), row = (e / (kD / 4)) % p.group, d = (e % (kD / 4)) * 4;
         float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, red_m[w * 16 + row]);
-        float o = 0.f, l = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
+        for (uint32_t s = 0; s < nsub; ++s) M = fmaxf(M, red_m[(s * p.hpc + h) * 16 + row]);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float l = 0.f;
+        for (uint32_t s = 0; s < nsub; ++s) {
+            const uint32_t w = s * p.hpc + h;
             const float mw = red_m[w * 16 + row];
             const float sc = mw == -INFINITY ? 0.f : exp2f(mw - M);
-            o += sc * red_o[(w * 16 + row) * kD + d];
+            const float4 v = *reinterpret_cast<const float4*>(&red_o[(w * 16 + row) * kRedStride + d]);
+            o.x += sc * v.x;
+            o.y += sc * v.y;
+            o.z += sc * v.z;
+            o.w += sc * v.w;
             l += sc * red_l[w * 16 + row];
         }
-        p.part_o[(pbase * p.group + row) * kD + d] = o;
-        if (d == 0) {
-            p.part_ml[(pbase * p.group + row) * 2] = M;
-            p.part_ml[(pbase * p.group + row) * 2 + 1] = l;
+        const uint32_t hg = blockIdx.y * p.hpc + h;
+        if (it.nsib == 1) {
+            const float r = l > 0.f ? 1.f / l : 0.f;
+            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(
+                p.out + ((static_cast<uint64_t>(it.seq) * p.hq + hg * p.group + row) * kD + d));
+            ob[0] = __floats2bfloat162_rn(o.x * r, o.y * r);
+            ob[1] = __floats2bfloat162_rn(o.z * r, o.w * r);
+        } else {
+            const uint64_t k = (static_cast<uint64_t>(blockIdx.x) * p.hkv + hg) * p.group + row;
+            *reinterpret_cast<float4*>(&p.part_o[k * kD + d]) = o;
+            if (d == 0) {
+                p.part_ml[k * 2] = M;
+                p.part_ml[k * 2 + 1] = l;
+            }
         }
     }
+    // partials are written: the combine kernel (PDL secondary) may start consuming
+    __syncthreads();
+    if (p.trace && tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-// out[b][hq][d] = sum_i e_i o_i / sum_i e_i l_i over the sequence's items, e_i = 2^(m_i - M)
-__global__ void __launch_bounds__(kD) kvf_attend_combine_kernel(const float* part_o, const float* part_ml,
-                                                                const uint32_t* seq_item0, uint32_t hkv,
-                                                                uint32_t group, __nv_bfloat16* out) {
-    const uint32_t b = blockIdx.x, hq = blockIdx.y, d = threadIdx.x;
-    const uint32_t head = hq / group, row = hq % group;
-    const uint32_t i0 = seq_item0[b], i1 = seq_item0[b + 1];
+// Merge a sequence's partials per (q head): out = sum_i e_i o_i / sum_i e_i l_i, e_i = 2^(m_i - M).
+// Launched as a programmatic dependent of the main kernel: griddepcontrol.wait releases it
+// once every CTA of the main kernel has published its partials.  One CTA per (sequence,
+// q head); its 8 warps split the partials (lane = 4 of the 128 dims), so a sequence cut into
+// ~150 items still merges in a few load round trips.
+constexpr int kCombWarps = 8;
+__global__ void __launch_bounds__(kCombWarps * 32) kvf_attend_combine_kernel(const float* part_o, const float* part_ml,
+                                                                            const uint32_t* seq_item0, uint32_t hkv,
+                                                                            uint32_t group, __nv_bfloat16* out) {
+    __shared__ float4 red_o[kCombWarps][32];
+    __shared__ float red_x[kCombWarps], red_l[kCombWarps];
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    const uint32_t b = blockIdx.x, hq = blockIdx.y;
+    const uint32_t i0 = seq_item0[b], n = seq_item0[b + 1] - i0;
+    if (n <= 1) return;  // written by the main kernel (or an empty sequence)
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, head = hq / group, row = hq % group;
+    auto key = [&](uint32_t i) { return (static_cast<uint64_t>(i0 + i) * hkv + head) * group + row; };
     float M = -INFINITY;
-    for (uint32_t i = i0; i < i1; ++i) M = fmaxf(M, part_ml[((static_cast<uint64_t>(i) * hkv + head) * group + row) * 2]);
-    float o = 0.f, l = 0.f;
-    for (uint32_t i = i0; i < i1; ++i) {
-        const uint64_t k = (static_cast<uint64_t>(i) * hkv + head) * group + row;
-        const float mi = part_ml[k * 2];
-        const float sc = mi == -INFINITY ? 0.f : exp2f(mi - M);
-        o += sc * part_o[k * kD + d];
-        l += sc * part_ml[k * 2 + 1];
+    for (uint32_t i = tid; i < n; i += kCombWarps * 32) M = fmaxf(M, part_ml[key(i) * 2]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) red_x[warp] = M;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kCombWarps; ++w) M = fmaxf(M, red_x[w]);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    float l = 0.f;
+#pragma unroll 4
+    for (uint32_t i = warp; i < n; i += kCombWarps) {
+        const uint64_t k = key(i);
+        const float2 ml = *reinterpret_cast<const float2*>(part_ml + k * 2);
+        const float sc = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+        const float4 v = reinterpret_cast<const float4*>(part_o + k * kD)[lane];
+        o.x += sc * v.x;
+        o.y += sc * v.y;
+        o.z += sc * v.z;
+        o.w += sc * v.w;
+        l += sc * ml.y;
     }
-    out[(static_cast<uint64_t>(b) * gridDim.y + hq) * kD + d] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
+    red_o[warp][lane] = o;
+    if (lane == 0) red_l[warp] = l;
+    __syncthreads();
+    if (warp) return;
+    o = red_o[0][lane];
+    l = red_l[0];
+#pragma unroll
+    for (int w = 1; w < kCombWarps; ++w) {
+        const float4 v = red_o[w][lane];
+        o.x += v.x;
+        o.y += v.y;
+        o.z += v.z;
+        o.w += v.w;
+        l += red_l[w];
+    }
+    const float r = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat162* ob =
+        reinterpret_cast<__nv_bfloat162*>(out + (static_cast<uint64_t>(b) * hkv * group + hq) * kD + lane * 4);
+    ob[0] = __floats2bfloat162_rn(o.x * r, o.y * r);
+    ob[1] = __floats2bfloat162_rn(o.z * r, o.w * r);
+}
+
+// sequences with no tokens: out = 0 (softmax over an empty set has no value)
+__global__ void kvf_attend_zero_kernel(const uint32_t* empty, uint32_t n, uint32_t hq, __nv_bfloat16* out) {
+    const uint64_t per = static_cast<uint64_t>(hq) * kD;
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n * per;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[empty[k / per] * per + k % per] = __float2bfloat16_rn(0.f);
 }
 
 }  // namespace
@@ -321,19 +429,40 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
         return set_error(KVF_E_INVALID_ARG, "kvf_decode_attend: head_dim 128, bf16 only");
     if (layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "layer out of range");
     if (group == 0 || group > kMaxGroup) return set_error(KVF_E_INVALID_ARG, "group must be 1..16");
+    if (chunk_tokens && (chunk_tokens % kTok || chunk_tokens > kMaxChunk))
+        return set_error(KVF_E_INVALID_ARG, "chunk_tokens must be a multiple of 16 in [16, 2048] (0 = auto)");
     if (batch == 0) return KVF_OK;
     if (!q || !out || !run_counts) return set_error(KVF_E_INVALID_ARG, "null q / out / run_counts");
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
     const uint32_t hkv = e->geom.kv_heads_local, hq = hkv * group;
+    const uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta));  // heads per CTA
+    const uint32_t ygrid = hkv / hpc;
+    if (ygrid > 65535 || batch >= (1u << 31) || hq > 65535)
+        return set_error(KVF_E_TOO_LARGE, "batch or head count too large");
 
-    // ---- flatten the run tables: per-run (token offset, slot), validated against the pool
-    uint64_t nruns = 0, total_tok = 0;
+    uint64_t nruns = 0;
     for (uint32_t b = 0; b < batch; ++b) nruns += run_counts[b];
     if (nruns && !runs) return set_error(KVF_E_INVALID_ARG, "null run list");
-    std::vector<uint32_t> rtok(nruns), rslot(nruns);
-    std::vector<uint32_t> seq_r0(batch + 1, 0);
-    std::vector<uint64_t> seq_len(batch, 0);
-    {
+    // ---- descriptor cache: a decode step calls K6 once per layer with the same run tables
+    std::vector<uint64_t> sig;
+    sig.reserve(4 + batch + 2 * nruns);
+    sig.push_back(batch);
+    sig.push_back(group);
+    sig.push_back(chunk_tokens);
+    for (uint32_t b = 0; b < batch; ++b) sig.push_back(run_counts[b]);
+    for (uint64_t k = 0; k < nruns; ++k) {
+        sig.push_back(runs[k].start);
+        sig.push_back(runs[k].len);
+    }
+    const bool hit = sig == e->att_sig;
+    uint64_t* meta = e->att_meta;  // nitems, total_tok, in_bytes, b_items, b_rt, b_rs, b_si, b_po, nempty, multi
+    Job j;
+    if (!hit) {
+        if (e->dev_slots >= (1ull << 32)) return set_error(KVF_E_TOO_LARGE, "pool beyond 2^32 slots");
+        // ---- flatten the run tables: per-run (token offset, slot), validated against the pool
+        uint64_t total_tok = 0;
+        std::vector<uint32_t> rtok(nruns), rslot(nruns), seq_r0(batch + 1, 0), empty;
+        std::vector<uint64_t> seq_len(batch, 0);
         uint64_t k = 0;
         for (uint32_t b = 0; b < batch; ++b) {
             seq_r0[b] = static_cast<uint32_t>(k);
@@ -349,69 +478,113 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
             if (t >= (1ull << 31)) return set_error(KVF_E_TOO_LARGE, "sequence longer than 2^31 tokens");
             seq_len[b] = t;
             total_tok += t;
+            if (t == 0) empty.push_back(b);
         }
         seq_r0[batch] = static_cast<uint32_t>(k);
-    }
-    if (e->dev_slots >= (1ull << 32)) return set_error(KVF_E_TOO_LARGE, "pool beyond 2^32 slots");
-    // ---- work items: <= chunk tokens and <= kMaxRuns runs each (chunk from the SM count)
-    uint32_t chunk = chunk_tokens;
-    if (chunk == 0) {
-        chunk = kMaxChunk;
-        const uint64_t want = static_cast<uint64_t>(e->sm_count) * 4;  // 2 CTAs/SM, 2 waves
-        while (chunk > kStageTok && ((total_tok + chunk - 1) / chunk) * hkv < want) chunk >>= 1;
-    }
-    if (chunk < kStageTok || chunk > kMaxChunk || chunk % kStageTok)
-        return set_error(KVF_E_INVALID_ARG, "chunk_tokens must be a multiple of 64 in [64, 1024] (0 = auto)");
-    std::vector<AttnItem> items;
-    std::vector<uint32_t> seq_item0(batch + 1, 0);
-    for (uint32_t b = 0; b < batch; ++b) {
-        seq_item0[b] = static_cast<uint32_t>(items.size());
-        uint32_t r = seq_r0[b];
-        const uint32_t rend = seq_r0[b + 1];
-        uint64_t t = 0;
-        while (t < seq_len[b]) {
-            while (r + 1 < rend && rtok[r + 1] <= t) ++r;  // run holding token t
-            uint64_t end = std::min<uint64_t>(seq_len[b], t + chunk);
-            const uint32_t rlast = std::min<uint32_t>(rend, r + kMaxRuns);  // runs [r, rlast) usable
-            if (rlast < rend) end = std::min<uint64_t>(end, rtok[rlast]);
-            uint32_t nr = 0;
-            while (r + nr < rend && rtok[r + nr] < end) ++nr;
-            items.push_back(AttnItem{b, static_cast<uint32_t>(t), static_cast<uint32_t>(end - t), r, nr, 0, 0, 0});
-            t = end;
+        // ---- work items: one wave of resident CTAs, balanced -- a decode layer is ~20 us of
+        // HBM time, so a second partial wave costs as much as the whole layer
+        if (!e->attend_occ) {
+            int occ = 0;
+            KVF_CUDA(cudaFuncSetAttribute(kvf_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kSmemBytes)));
+            KVF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kvf_attend_kernel, kThreads, kSmemBytes));
+            e->attend_occ = std::max(1, occ);
+            e->attend_attr_set = true;
         }
-    }
-    seq_item0[batch] = static_cast<uint32_t>(items.size());
-    const uint64_t nitems = items.size();
-    if (nitems > 0x7fffffffull) return set_error(KVF_E_TOO_LARGE, "too many work items");
+        std::vector<uint64_t> kseq(batch, 0);  // items per sequence
+        if (chunk_tokens) {
+            for (uint32_t b = 0; b < batch; ++b) kseq[b] = (seq_len[b] + chunk_tokens - 1) / chunk_tokens;
+        } else if (total_tok) {
+            const uint64_t slots = static_cast<uint64_t>(e->sm_count) * e->attend_occ;
+            // >= 64 tokens per item: below that the CTA prologue outweighs its bytes
+            const double T = std::max(64.0, static_cast<double>(total_tok) * ygrid / static_cast<double>(slots));
+            uint64_t used = 0;
+            for (uint32_t b = 0; b < batch; ++b) {
+                if (!seq_len[b]) continue;
+                kseq[b] = std::max<uint64_t>({1, static_cast<uint64_t>(seq_len[b] / T),
+                                              (seq_len[b] + kMaxChunk - 1) / kMaxChunk});
+                used += kseq[b] * ygrid;
+            }
+            // spend what is left of the wave on the sequences with the largest items
+            std::priority_queue<std::pair<double, uint32_t>> pq;
+            for (uint32_t b = 0; b < batch; ++b)
+                if (seq_len[b] >= 64 * (kseq[b] + 1)) pq.push({static_cast<double>(seq_len[b]) / kseq[b], b});
+            while (used + ygrid <= slots && !pq.empty()) {
+                const uint32_t b = pq.top().second;
+                pq.pop();
+                ++kseq[b];
+                used += ygrid;
+                if (seq_len[b] >= 64 * (kseq[b] + 1)) pq.push({static_cast<double>(seq_len[b]) / kseq[b], b});
+            }
+        }
+        std::vector<AttnItem> items;
+        std::vector<uint32_t> seq_item0(batch + 1, 0);
+        bool multi = false;
+        for (uint32_t b = 0; b < batch; ++b) {
+            seq_item0[b] = static_cast<uint32_t>(items.size());
+            if (!seq_len[b]) continue;
+            const uint64_t kb = kseq[b];
+            const uint64_t per = std::min<uint64_t>(kMaxChunk, ((seq_len[b] + kb - 1) / kb + kTok - 1) / kTok * kTok);
+            const size_t first = items.size();
+            uint32_t r = seq_r0[b];
+            const uint32_t rend = seq_r0[b + 1];
+            uint64_t t = 0;
+            while (t < seq_len[b]) {
+                while (r + 1 < rend && rtok[r + 1] <= t) ++r;  // run holding token t
+                uint64_t end = std::min<uint64_t>(seq_len[b], t + per);
+                if (r + kMaxRuns < rend) end = std::min<uint64_t>(end, rtok[r + kMaxRuns]);
+                uint32_t nr = 0;
+                while (r + nr < rend && rtok[r + nr] < end) ++nr;
+                items.push_back(AttnItem{b, static_cast<uint32_t>(t), static_cast<uint32_t>(end - t), r, nr, 0, 0, 0});
+                t = end;
+            }
+            for (size_t i = first; i < items.size(); ++i) items[i].nsib = static_cast<uint32_t>(items.size() - first);
+            multi |= items.size() - first > 1;
+        }
+        seq_item0[batch] = static_cast<uint32_t>(items.size());
+        const uint64_t nitems = items.size();
+        if (nitems > 0x7fffffffull) return set_error(KVF_E_TOO_LARGE, "too many work items");
 
-    // ---- device blob: items | run_tok | run_slot | seq_item0 | partials (o, ml)
-    auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
-    const size_t b_items = al(nitems * sizeof(AttnItem)), b_rt = al(nruns * 4), b_rs = al(nruns * 4),
-                 b_si = al((batch + 1) * 4);
-    const size_t b_po = al(nitems * hkv * group * kD * 4), b_pm = al(nitems * hkv * group * 2 * 4);
-    const size_t in_bytes = b_items + b_rt + b_rs + b_si;
-    Job j;
-    // grow the workspace only between calls: cudaFree must not race an in-flight reader
-    if (in_bytes + b_po + b_pm > e->ws_att.dev_bytes || in_bytes > e->ws_att.host_bytes) {
-        KVF_CUDA(cudaStreamSynchronize(e->s_cmp));
-        e->att_upload_pending = false;
-        if (int rc = e->ws_att.ensure(in_bytes + b_po + b_pm, in_bytes)) return rc;
+        // ---- device blob: items | run_tok | run_slot | seq_item0 | empty seqs | partials (o, ml)
+        auto al = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+        const size_t b_items = al(nitems * sizeof(AttnItem)), b_rt = al(nruns * 4), b_rs = al(nruns * 4),
+                     b_si = al((batch + 1) * 4), b_em = al(empty.size() * 4);
+        const size_t b_po = multi ? al(nitems * hkv * group * kD * 4) : 0;
+        const size_t b_pm = multi ? al(nitems * hkv * group * 2 * 4) : 0;
+        const size_t in_bytes = b_items + b_rt + b_rs + b_si + b_em;
+        const size_t dev_need = in_bytes + b_po + b_pm;
+        // grow the workspace only between calls: cudaFree must not race an in-flight reader
+        if (dev_need > e->ws_att.dev_bytes || in_bytes > e->ws_att.host_bytes) {
+            KVF_CUDA(cudaStreamSynchronize(e->s_cmp));
+            e->att_upload_pending = false;
+            if (int rc = e->ws_att.ensure(dev_need, in_bytes)) return rc;
+        }
+        // the pinned staging may still feed the previous call's upload: wait for that copy only
+        if (e->att_upload_pending) KVF_CUDA(cudaEventSynchronize(e->att_upload_done));
+        char* hs = static_cast<char*>(e->ws_att.host);
+        std::memcpy(hs, items.data(), nitems * sizeof(AttnItem));
+        std::memcpy(hs + b_items, rtok.data(), nruns * 4);
+        std::memcpy(hs + b_items + b_rt, rslot.data(), nruns * 4);
+        std::memcpy(hs + b_items + b_rt + b_rs, seq_item0.data(), (batch + 1) * 4);
+        std::memcpy(hs + b_items + b_rt + b_rs + b_si, empty.data(), empty.size() * 4);
+        e->att_sig.clear();  // invalid until the upload below is enqueued
+        int rc = begin_job(e, job_id, e->s_cmp, j);
+        if (rc) return rc;
+        KVF_CUDA(cudaMemcpyAsync(e->ws_att.dev, hs, in_bytes, cudaMemcpyHostToDevice, e->s_cmp));
+        KVF_CUDA(cudaEventRecord(e->att_upload_done, e->s_cmp));
+        e->att_upload_pending = true;
+        e->att_sig.swap(sig);
+        const uint64_t m[10] = {nitems, total_tok, in_bytes, b_items, b_rt, b_rs, b_si, b_po, empty.size(), multi};
+        std::copy(m, m + 10, meta);
+    } else {
+        int rc = begin_job(e, job_id, e->s_cmp, j);
+        if (rc) return rc;
     }
-    // the pinned staging may still feed the previous call's upload: wait for that copy only
-    if (e->att_upload_pending) KVF_CUDA(cudaEventSynchronize(e->att_upload_done));
-    char* hs = static_cast<char*>(e->ws_att.host);
-    std::memcpy(hs, items.data(), nitems * sizeof(AttnItem));
-    std::memcpy(hs + b_items, rtok.data(), nruns * 4);
-    std::memcpy(hs + b_items + b_rt, rslot.data(), nruns * 4);
-    std::memcpy(hs + b_items + b_rt + b_rs, seq_item0.data(), (batch + 1) * 4);
-    char* ds = static_cast<char*>(e->ws_att.dev);
-    int rc = begin_job(e, job_id, e->s_cmp, j);
-    if (rc) return rc;
     // KV written by fills / K3 scatters on the dev stream must be visible to the reads
     if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_cmp, e->dev_write_done, 0));
-    KVF_CUDA(cudaMemcpyAsync(ds, hs, in_bytes, cudaMemcpyHostToDevice, e->s_cmp));
-    KVF_CUDA(cudaEventRecord(e->att_upload_done, e->s_cmp));
-    e->att_upload_pending = true;
+    const uint64_t nitems = meta[0], total_tok = meta[1], in_bytes = meta[2], b_items = meta[3], b_rt = meta[4],
+                   b_rs = meta[5], b_si = meta[6], b_po = meta[7], nempty = meta[8], multi = meta[9];
+    char* ds = static_cast<char*>(e->ws_att.dev);
 
     AttnParams prm{};
     prm.pool = e->dev_pool;
@@ -420,12 +593,16 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
     prm.layer = layer;
     prm.group = group;
     prm.hq = hq;
+    prm.hkv = hkv;
+    prm.hpc = hpc;
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.q = static_cast<const __nv_bfloat16*>(q);
+    prm.out = static_cast<__nv_bfloat16*>(out);
     prm.items = reinterpret_cast<const AttnItem*>(ds);
     prm.run_tok = reinterpret_cast<const uint32_t*>(ds + b_items);
     prm.run_slot = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt);
     const uint32_t* d_seq_item0 = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt + b_rs);
+    const uint32_t* d_empty = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt + b_rs + b_si);
     prm.part_o = reinterpret_cast<float*>(ds + in_bytes);
     prm.part_ml = reinterpret_cast<float*>(ds + in_bytes + b_po);
     if (!e->attend_attr_set) {
@@ -433,15 +610,51 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
                                       static_cast<int>(kSmemBytes)));
         e->attend_attr_set = true;
     }
+    static const char* trace_path = std::getenv("KVF_ATTEND_TRACE");
+    unsigned long long* d_trace = nullptr;
+    if (trace_path && nitems) {
+        KVF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), nitems * ygrid * 5 * 8, e->s_cmp));
+        prm.trace = d_trace;
+    }
     if (nitems) {
-        kvf_attend_kernel<<<dim3(static_cast<uint32_t>(nitems), hkv), kThreads, kSmemBytes, e->s_cmp>>>(prm);
+        kvf_attend_kernel<<<dim3(static_cast<uint32_t>(nitems), ygrid), kThreads, kSmemBytes, e->s_cmp>>>(prm);
         KVF_CUDA(cudaGetLastError());
         e->stats.kernel_launches++;
     }
-    kvf_attend_combine_kernel<<<dim3(batch, hq), kD, 0, e->s_cmp>>>(prm.part_o, prm.part_ml, d_seq_item0, hkv, group,
-                                                                   static_cast<__nv_bfloat16*>(out));
-    KVF_CUDA(cudaGetLastError());
-    e->stats.kernel_launches++;
+    if (multi) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(batch, hq);
+        cfg.blockDim = dim3(kCombWarps * 32);
+        cfg.stream = e->s_cmp;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        KVF_CUDA(cudaLaunchKernelEx(&cfg, kvf_attend_combine_kernel, static_cast<const float*>(prm.part_o),
+                                    static_cast<const float*>(prm.part_ml), d_seq_item0, hkv, group, prm.out));
+        e->stats.kernel_launches++;
+    }
+    if (nempty) {
+        kvf_attend_zero_kernel<<<static_cast<uint32_t>(std::min<uint64_t>(1024, (nempty * hq * kD + 255) / 256)), 256, 0,
+                                 e->s_cmp>>>(d_empty, static_cast<uint32_t>(nempty), hq, prm.out);
+        KVF_CUDA(cudaGetLastError());
+        e->stats.kernel_launches++;
+    }
+    if (d_trace) {  // diagnostics only: synchronous dump, one line per call
+        std::vector<unsigned long long> tr(nitems * ygrid * 5);
+        KVF_CUDA(cudaMemcpyAsync(tr.data(), d_trace, tr.size() * 8, cudaMemcpyDeviceToHost, e->s_cmp));
+        KVF_CUDA(cudaStreamSynchronize(e->s_cmp));
+        KVF_CUDA(cudaFree(d_trace));
+        if (FILE* f = std::fopen(trace_path, "a")) {
+            std::fprintf(f, "[");
+            for (size_t i = 0; i < tr.size(); i += 5)
+                std::fprintf(f, "%s[%llu,%llu,%llu,%llu,%llu]", i ? "," : "", tr[i], tr[i + 1], tr[i + 2], tr[i + 3],
+                             tr[i + 4]);
+            std::fprintf(f, "]\n");
+            std::fclose(f);
+        }
+    }
     j.bytes = total_tok * 2 * e->tpb;  // K + V of one layer, read once
     e->stats.attend_bytes += j.bytes;
     e->stats.attend_calls++;

@@ -115,6 +115,9 @@ struct kvf_engine {
     kvf_impl::Workspace ws_att;  // K6 decode attention: descriptors + partials (s_cmp)
     cudaEvent_t att_upload_done = nullptr;  // last K6 descriptor upload out of ws_att.host
     bool att_upload_pending = false, attend_attr_set = false;
+    int attend_occ = 0;  // resident K6 CTAs per SM
+    std::vector<uint64_t> att_sig;  // K6 descriptor cache: inputs of the blob now in ws_att.dev
+    uint64_t att_meta[10] = {};     //   and its sizes (a decode step calls K6 once per layer)
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
     std::map<uint64_t, kvf_impl::BigGraph> big_graphs;  // key: bucket << 1 | workflow_aware
 

@@ -163,14 +163,22 @@ class Engine:
         N.check(self._lib.kvf_dev_scatter(self.h, job, staging_ptr, N.runs_array(dev_runs), len(dev_runs)))
         return job
 
+    @staticmethod
+    def attend_runs(seq_runs):
+        """Pack per-sequence run lists once (a decode step reuses them for every layer)."""
+        flat = np.array([r for runs in seq_runs for r in runs] or [(0, 0)], dtype=np.uint64).reshape(-1, 2)
+        counts = np.array([len(r) for r in seq_runs], dtype=np.uint32)
+        return flat, counts
+
     def attend(self, layer, group, q_ptr, seq_runs, out_ptr, scale, job=None, chunk=0):
         """K6: decode attention of layer `layer` over each sequence's slot runs, in place
-        (q/out: device bf16 [batch][kv_heads_local*group][128]).  Async job on the compute stream."""
+        (q/out: device bf16 [batch][kv_heads_local*group][128]).  Async job on the compute stream.
+        seq_runs: list of run lists, or the tuple attend_runs() returned."""
         job = job or self.new_job()
-        flat = [r for runs in seq_runs for r in runs]
-        counts = np.array([len(r) for r in seq_runs], dtype=np.uint32)
-        N.check(self._lib.kvf_decode_attend(self.h, job, layer, len(seq_runs), group, q_ptr, N.runs_array(flat),
-                                            counts.ctypes.data, float(scale), out_ptr, chunk))
+        flat, counts = seq_runs if isinstance(seq_runs, tuple) else self.attend_runs(seq_runs)
+        N.check(self._lib.kvf_decode_attend(self.h, job, layer, len(counts), group, q_ptr,
+                                            C.cast(flat.ctypes.data, C.POINTER(N.Run)), counts.ctypes.data,
+                                            float(scale), out_ptr, chunk))
         return job
 
     def query(self, job):

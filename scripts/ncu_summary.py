@@ -18,6 +18,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns"
         "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9, "second": 1.0}
 ALGO = {  # algorithmic bytes per launch of the capture in scripts/profile_kernels.py
     "k1": 8192 * 131072, "k2": 128 * 131072, "k3": 2 * 8192 * 131072,
+    "k6": 4 * 8320 * 2 * 2048,  # one layer of 4 x 8320-token sequences, K + V (scripts/attend_bench.py --ncu)
 }
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__grid_size",
         "launch__block_size", "launch__registers_per_thread", "pcie__read_bytes.sum.per_second",

@@ -76,7 +76,7 @@ def check(out, ref):
     assert err.mean().item() <= MEAN_TOL, err.mean().item()
 
 
-@pytest.mark.parametrize("kv_local,group,chunk", [(8, 4, 0), (8, 4, 64), (8, 4, 1024), (2, 8, 0), (1, 8, 128),
+@pytest.mark.parametrize("kv_local,group,chunk", [(8, 4, 0), (8, 4, 16), (8, 4, 64), (8, 4, 2048), (2, 8, 0), (1, 8, 128),
                                                   (8, 1, 256), (4, 16, 0)])
 def test_attend_ragged_fragmented(kv_local, group, chunk):
     need_gpu()
