@@ -34,8 +34,9 @@ constexpr int64_t kRankUnreachable = INT64_MAX / 4;
 constexpr uint32_t kMaxNodesSingleCta = 4096;
 constexpr int kThreads = 1024;
 constexpr int32_t kBlocked = INT32_MAX;
-// K5 result header: [count, immediate, pending, 6 globaltimer stamps, 6 clock64 stamps]
+// K5 result header: [count, immediate, pending, 6 globaltimer stamps, 6 clock64 stamps, done seq]
 constexpr size_t kHeaderBytes = 128;
+constexpr int kDoneWord = 15;  // the host spins on header[15] == call sequence number
 // decision inputs up to this size are read by the kernel straight from mapped pinned memory
 constexpr size_t kZeroCopyBytes = 64 << 10;
 
@@ -66,10 +67,28 @@ __device__ __forceinline__ const T* rebase(const T* p, const uint8_t* from, cons
 // staged there too (stage_blob), so the root walks never touch PCIe-mapped host memory.
 constexpr uint32_t kPrioSmemNodes = 4096;
 
+// Publish a decision kernel's result to a host spinning on mapped memory: every thread fences
+// its own output stores system-wide, then one thread writes the call's sequence number.
+__device__ __forceinline__ void publish_done(unsigned long long* flag, unsigned long long seq) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && flag) {
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* parent, uint32_t n, const int32_t* bidx,
                                                                 const int64_t* cand, uint32_t m, long long* out,
-                                                                const uint8_t* blob, uint32_t blob_bytes) {
+                                                                const uint8_t* blob, uint32_t blob_bytes,
+                                                                unsigned long long* hdr, unsigned long long seq) {
     extern __shared__ __align__(16) uint8_t psm[];
+    const unsigned long long t_begin = gtimer();
     const bool staged = n <= kPrioSmemNodes;
     long long* rank = reinterpret_cast<long long*>(psm);
     if (blob_bytes) {  // inputs -> shared memory in one round trip
@@ -90,6 +109,11 @@ __global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* p
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = rank[i];
     }
+    if (hdr && threadIdx.x == 0) {
+        hdr[3] = t_begin;
+        hdr[8] = gtimer();
+    }
+    publish_done(hdr ? hdr + kDoneWord : nullptr, seq);
 }
 
 struct TreeDev {
@@ -120,6 +144,7 @@ struct OutDev {
     int32_t* idx;
     uint8_t* action;
     unsigned long long* header;  // [count, immediate, pending, 6 phase stamps] (kHeaderBytes)
+    bool spin;                   // header is mapped host memory the caller spins on
 };
 
 // Warp-aggregated slot claim on a shared counter: one atomic per warp instead of per lane.
@@ -197,7 +222,8 @@ __device__ __forceinline__ uint64_t time_order(double t) {
 // Everything the later phases touch is staged here once, so inputs may live in mapped host
 // memory (small trees) without per-phase PCIe round trips.
 // flags: bit0 selfok, bit1 releases, bit2 R
-__global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in, const ReqDev q, OutDev o) {
+__global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in, const ReqDev q, OutDev o,
+                                                              unsigned long long seq) {
     extern __shared__ __align__(16) uint8_t sm[];
     TreeDev t = t_in;
     const uint32_t n = t.n;
@@ -477,6 +503,7 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
         o.header[2] = s_pend;
     }
     stamp(5);
+    publish_done(o.spin ? o.header + kDoneWord : nullptr, seq);
 }
 
 size_t victim_smem(uint32_t n, size_t blob = 0) {
@@ -494,6 +521,31 @@ int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
     float ms = 0;
     KVF_CUDA(cudaEventElapsedTime(&ms, e->dec_start, e->dec_stop));
     e->stats.decision_kernel_ms += ms;
+    e->stats.decision_call_us +=
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    return KVF_OK;
+}
+
+// Fast-path completion: the kernel publishes `seq` into mapped pinned memory after its
+// outputs (publish_done); the host spins on it instead of cudaStreamSynchronize -- the
+// result is usable one posted PCIe write after the kernel's last store.  A fault surfaces
+// through the periodic cudaStreamQuery.  Kernel time comes from its own globaltimer stamps.
+int spin_decision(kvf_engine* e, const unsigned long long* hdr, unsigned long long seq,
+                  std::chrono::steady_clock::time_point t0) {
+    const volatile unsigned long long* flag = hdr + kDoneWord;
+    for (uint32_t it = 1;; ++it) {
+        if (__atomic_load_n(const_cast<const unsigned long long*>(flag), __ATOMIC_ACQUIRE) == seq) break;
+        if ((it & 255) == 0) {
+            const cudaError_t st = cudaStreamQuery(e->s_dec);
+            if (st != cudaSuccess && st != cudaErrorNotReady) return cuda_error(st, "decision kernel");
+            if (st == cudaSuccess && __atomic_load_n(const_cast<const unsigned long long*>(flag), __ATOMIC_ACQUIRE) != seq)
+                return set_error(KVF_E_INTERNAL, "decision kernel finished without publishing its result");
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    e->stats.decision_kernel_ms += static_cast<double>(hdr[8] - hdr[3]) * 1e-6;
     e->stats.decision_call_us +=
         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     return KVF_OK;
@@ -522,7 +574,7 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
         if (bidx[b] < 0 || static_cast<uint32_t>(bidx[b]) >= n) return set_error(KVF_E_UNKNOWN_BOUNDARY_NODE, "boundary index out of range");
     const size_t in_bytes = ((n * 4 + 15) & ~15ull) + ((m * 4 + 15) & ~15ull) + ((m * 8 + 15) & ~15ull);
     const size_t out_bytes = n * 8;
-    int rc = e->ws_dec.ensure(in_bytes + out_bytes + 1024, in_bytes + out_bytes + 1024);
+    int rc = e->ws_dec.ensure(in_bytes + out_bytes + 1024 + 512, in_bytes + out_bytes + 1024 + 512);
     if (rc) return rc;
     char* h = static_cast<char*>(e->ws_dec.host);
     char* hp = h;
@@ -540,8 +592,13 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     int32_t* d_bidx = carve<int32_t>(dp, m);
     int64_t* d_cand = carve<int64_t>(dp, m);
     long long* d_out = reinterpret_cast<long long*>(base + out_off);
+    // header (stamps + done word) after the ranks, in mapped memory on the fast path
+    const size_t hdr_off = (out_off + n * 8 + 255) & ~size_t(255);
+    unsigned long long* h_hdr = reinterpret_cast<unsigned long long*>(h + hdr_off);
+    unsigned long long* d_hdr = zero_copy ? reinterpret_cast<unsigned long long*>(base + hdr_off) : nullptr;
+    const unsigned long long seq = ++e->dec_seq;
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
-    KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
+    if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_copy ? used : 0);
     if (!e->prio_attr_set) {
         KVF_CUDA(cudaFuncSetAttribute(kvf_priority_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -550,12 +607,17 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     }
     kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
                                                          zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
-                                                         zero_copy ? static_cast<uint32_t>(used) : 0u);
+                                                         zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq);
     KVF_CUDA(cudaGetLastError());
-    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;
-    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(h + out_off, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
+    if (zero_copy) {
+        if (int src = spin_decision(e, h_hdr, seq, t0)) return src;
+        std::memcpy(out_rank, h + out_off, n * 8);
+        return KVF_OK;
+    }
+    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
+    KVF_CUDA(cudaMemcpyAsync(h + out_off, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
     KVF_CUDA(cudaStreamSynchronize(e->s_dec));
     std::memcpy(out_rank, h + out_off, n * 8);
     return finish_decision(e, t0);
@@ -628,18 +690,24 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
                                       static_cast<int>(victim_smem(kMaxNodesSingleCta))));
         e->victim_attr_set = true;
     }
-    KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
-    kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od);
+    od.spin = zero_copy;
+    const unsigned long long seq = ++e->dec_seq;
+    if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
+    kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od, seq);
     if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess)
         return cuda_error(le, ("K5 launch (n=" + std::to_string(n) + " threads=" + std::to_string(victim_threads(n)) +
                                " smem=" + std::to_string(smem) + " zero_copy=" + std::to_string(zero_copy) + ")")
                                   .c_str());
-    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
     e->stats.kernel_launches++;
     e->stats.decisions++;
     char* hout = h + ((used + 255) & ~size_t(255));
-    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));
-    KVF_CUDA(cudaStreamSynchronize(e->s_dec));
+    if (zero_copy) {
+        if (int src = spin_decision(e, reinterpret_cast<const unsigned long long*>(hout), seq, t0)) return src;
+    } else {
+        KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
+        KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));
+        KVF_CUDA(cudaStreamSynchronize(e->s_dec));
+    }
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
     for (int k = 0; k < 5; ++k) {
@@ -651,7 +719,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     *out_count = cnt;
     *out_imm = hdr[1];
     *out_pend = hdr[2];
-    return finish_decision(e, t0);
+    return zero_copy ? KVF_OK : finish_decision(e, t0);
 }
 
 }  // extern "C"

@@ -104,7 +104,8 @@ struct kvf_engine {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr, s_dev = nullptr, s_dec = nullptr;
     cudaStream_t s_cmp = nullptr;  // emulated model compute (kvf_compute_*): never behind a fill
     cudaEvent_t dev_write_done = nullptr;  // last fill / K3 scatter on s_dev
-    cudaEvent_t dec_start = nullptr, dec_stop = nullptr;  // decision kernel timing
+    cudaEvent_t dec_start = nullptr, dec_stop = nullptr;  // decision kernel timing (copy path)
+    unsigned long long dec_seq = 0;  // decision calls: the done word the fast path spins on
     bool dev_write_pending = false;
 
     std::unordered_map<uint64_t, kvf_impl::Job> jobs;
