@@ -277,12 +277,40 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
         }
     }
 
-    // ---- merge the warps of each head in shared memory (the rings are free once all are here)
 #pragma unroll
     for (int o = 1; o <= 2; o <<= 1) {
         l0 += __shfl_xor_sync(0xffffffffu, l0, o);
         l1 += __shfl_xor_sync(0xffffffffu, l1, o);
     }
+    if (nsub == 1) {  // one warp per head (8 local heads): write straight from the accumulators
+        const uint64_t rowbase = static_cast<uint64_t>(it.seq) * p.hq + head * p.group;
+        const uint64_t pk = (static_cast<uint64_t>(blockIdx.x) * p.hkv + head) * p.group;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const uint32_t row = g + 8 * half;
+            if (row >= p.group) continue;
+            const float l = half ? l1 : l0, m = half ? m1 : m0;
+            const float r = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                const uint32_t d = n * 8 + cq;
+                const float a = acc[n][2 * half], b = acc[n][2 * half + 1];
+                if (it.nsib == 1)
+                    *reinterpret_cast<__nv_bfloat162*>(p.out + (rowbase + row) * kD + d) = __floats2bfloat162_rn(a * r, b * r);
+                else
+                    *reinterpret_cast<float2*>(&p.part_o[(pk + row) * kD + d]) = make_float2(a, b);
+            }
+            if (it.nsib != 1 && (lane & 3) == 0) {
+                p.part_ml[(pk + row) * 2] = m;
+                p.part_ml[(pk + row) * 2 + 1] = l;
+            }
+        }
+        __syncthreads();
+        if (p.trace && tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
+        asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        return;
+    }
+    // ---- merge the warps of each head in shared memory (the rings are free once all are here)
     __syncthreads();
     // [warp][16 rows][kRedStride]: the 8-float pad puts the 8 row groups of a float2 store in
     // distinct banks (2 wavefronts per store instead of 8); rows >= group are never stored

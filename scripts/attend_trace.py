@@ -27,10 +27,13 @@ torch.cuda.synchronize()
 if os.path.exists(path):
     os.remove(path)
 plan = e.attend_runs(seqs)
+jobs_ms = []
 for layer in range(6):
     j = e.attend(layer, 4, q.data_ptr(), plan, out.data_ptr(), 0.088)
     e.wait(j)
+    jobs_ms.append(e.elapsed_ms(j) * 1e3)
     e.release(j)
+print("job us (events: kernel + combine):", [round(x, 1) for x in jobs_ms])
 rows = [json.loads(l) for l in open(path)]
 tb = sum(lens) * 2 * e.tpb
 for call in rows[2:]:
