@@ -597,6 +597,9 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     unsigned long long* h_hdr = reinterpret_cast<unsigned long long*>(h + hdr_off);
     unsigned long long* d_hdr = zero_copy ? reinterpret_cast<unsigned long long*>(base + hdr_off) : nullptr;
     const unsigned long long seq = ++e->dec_seq;
+    // the done word sits wherever this call's n puts it -- possibly on bytes an earlier call
+    // left there (victim indices can equal a sequence number): clear it before the launch
+    if (zero_copy) __atomic_store_n(h_hdr + kDoneWord, 0ull, __ATOMIC_RELEASE);
     if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
     if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_copy ? used : 0);
@@ -692,6 +695,9 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     }
     od.spin = zero_copy;
     const unsigned long long seq = ++e->dec_seq;
+    if (zero_copy)  // see kvf_priority_propagate: never spin on a stale word
+        __atomic_store_n(reinterpret_cast<unsigned long long*>(h + ((used + 255) & ~size_t(255))) + kDoneWord, 0ull,
+                         __ATOMIC_RELEASE);
     if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
     kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od, seq);
     if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess)
