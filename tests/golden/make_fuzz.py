@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 TRACE = os.path.join(ROOT, "oracle", "_ref", "ref_trace")
 
 
-def draw(rng):
+def draw(rng, geom="micro"):
     topo = rng.choice(["CYCLIC", "SEQUENTIAL", "BRANCH_MAX", "BRANCH_MIN", "PEER_STYLE"])
     agents = 4 if topo.startswith("BRANCH") else rng.randint(1, 4)  # workload.cpp:35-36
     fixed = rng.choice([16, 32, 64, 96, 128, 256, 512])
@@ -57,6 +57,12 @@ def draw(rng):
         for k in ("fixed", "dyn", "out", "shared_prefix"):
             a.pop(k)
         a["gpu_cap"] = int(agents * workflows * 900 * 16 * rng.uniform(0.5, 2.0)) // 16 * 16
+    if geom == "llama8b":  # real KV bytes: every transfer is megabytes of K1/K2
+        scale = 131072 // 16
+        a.update(profile="h100-qwen32b", bpt=131072, vocab=32000)
+        a["gpu_cap"] *= scale
+        if "cpu_cap" in a:
+            a["cpu_cap"] *= scale
     return a
 
 
@@ -65,23 +71,27 @@ def main():
     ap.add_argument("--n", type=int, default=40)
     ap.add_argument("--seed", type=int, default=2507)
     ap.add_argument("--n-err", type=int, default=12)
+    ap.add_argument("--geom", choices=["micro", "llama8b"], default="micro",
+                    help="micro: 16 B/token, micro cost profile (sim_f_/sim_e_); llama8b: 128 KiB/token, "
+                         "h100-qwen32b profile, shorter prompts (sim_g_)")
     args = ap.parse_args()
     subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True, capture_output=True)
     out_dir = os.path.join(HERE, "fuzz")
     os.makedirs(out_dir, exist_ok=True)
+    pre = ("sim_g_",) if args.geom == "llama8b" else ("sim_f_", "sim_e_")
     for f in os.listdir(out_dir):
-        if f.startswith("sim_f_") or f.startswith("sim_e_"):
+        if f.startswith(pre):
             os.remove(os.path.join(out_dir, f))
     rng = random.Random(args.seed)
     kept, errs, rejected, tries = [], [], {}, 0
     while len(kept) < args.n and tries < 20 * args.n:
         tries += 1
-        a = draw(rng)
+        a = draw(rng, args.geom)
         r = subprocess.run([TRACE, "sim", *[f"{k}={v}" for k, v in a.items()]], capture_output=True, text=True)
         if r.returncode != 0:
             key = r.stderr.strip().split(":")[0] or f"rc {r.returncode}"
             rejected[key] = rejected.get(key, 0) + 1
-            if r.returncode == 3 and key.startswith("SimError") and len(errs) < args.n_err:
+            if r.returncode == 3 and key.startswith("SimError") and len(errs) < args.n_err and args.geom == "micro":
                 name = f"sim_e_{len(errs):02d}.jsonl"
                 code = int(key.split()[1])
                 with open(os.path.join(out_dir, name), "w") as f:
@@ -93,11 +103,11 @@ def main():
         n_job = sum(1 for l in lines if '"t":"job"' in l)
         if n_job == 0 and rng.random() < 0.7:  # keep the corpus transfer-heavy
             continue
-        name = f"sim_f_{len(kept):02d}.jsonl"
+        name = f"{'sim_g_' if args.geom == 'llama8b' else 'sim_f_'}{len(kept):02d}.jsonl"
         with open(os.path.join(out_dir, name), "w") as f:
             f.write(r.stdout)
         kept.append({"file": name, "args": a, "transitions": n_tr, "jobs": n_job})
-    with open(os.path.join(out_dir, "MANIFEST.json"), "w") as f:
+    with open(os.path.join(out_dir, f"MANIFEST{'_llama8b' if args.geom == 'llama8b' else ''}.json"), "w") as f:
         json.dump({"seed": args.seed, "tries": tries, "kept": kept, "errors": errs, "reference_rejected": rejected}, f,
                   indent=1)
     print(f"kept {len(kept)} of {tries}; reference rejected {rejected}; {len(errs)} error fixtures")
