@@ -333,6 +333,11 @@ def run_ours(args, rank, world, local):
                     "decision_us_max": round(res["decision_us_max"], 2),
                     "k4_us_per_call": round(res["priority_us"] / max(1, res["priority_calls"]), 2),
                     "k5_us_per_call": round(res["evict_us"] / max(1, res["evict_calls"]), 2),
+                    # the same calls as the engine timed them: C-ABI round trip and in-kernel time
+                    "engine_call_us_per_decision": round(res["engine_decision_call_us"] /
+                                                         max(1, res["engine_decisions"]), 2),
+                    "engine_kernel_us_per_decision": round(1e3 * res["engine_decision_kernel_ms"] /
+                                                           max(1, res["engine_decisions"]), 2),
                     "prefetch_ms_per_step": round(k1_avg, 3),
                     "reference_modelled_prefetch_ms": round(1e3 * ((1 << 30) / (64e9 * 0.6) + 50e-6), 3)},
         "gpu_launches": int(launches),

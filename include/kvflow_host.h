@@ -77,6 +77,10 @@ typedef struct {
     /* stalls (RequestTrace::stall_seconds, virtual seconds) over measured requests */
     double stall_total_s;
     uint64_t stalled_requests, measured_requests;
+    /* decision calls as the engine saw them (kvf_get_stats): in-kernel time (globaltimer) and
+       C-ABI call time, K4 + K5 together -- the rest of priority_us / evict_us is host packing */
+    uint64_t engine_decisions;
+    double engine_decision_kernel_ms, engine_decision_call_us;
 } kvfh_sim_result;
 
 const char* kvfh_last_error(void);

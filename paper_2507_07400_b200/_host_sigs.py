@@ -33,6 +33,8 @@ class SimResult(C.Structure):
         ("verify_failures", C.c_uint64), ("audits", C.c_uint64), ("d2h_batches", C.c_uint64),
         ("stall_total_s", C.c_double),
         ("stalled_requests", C.c_uint64), ("measured_requests", C.c_uint64),
+        ("engine_decisions", C.c_uint64), ("engine_decision_kernel_ms", C.c_double),
+        ("engine_decision_call_us", C.c_double),
     ]
 
 

@@ -277,7 +277,11 @@ int kvfh_sim_result_get(const kvfh_sim* s, kvfh_sim_result* r) {
         r->evict_calls = d.evict_calls;
         r->priority_us = d.priority_us;
         r->evict_us = d.evict_us;
-        r->kernel_launches = s->engine->stats().kernel_launches;
+        const kvf_stats es = s->engine->stats();
+        r->kernel_launches = es.kernel_launches;
+        r->engine_decisions = es.decisions;
+        r->engine_decision_kernel_ms = es.decision_kernel_ms;
+        r->engine_decision_call_us = es.decision_call_us;
         r->verified_loads = s->sim->verified_loads;
         r->verify_failures = s->sim->verify_failures;
         r->audits = s->audits;
