@@ -443,12 +443,6 @@ __global__ void kvf_attend_zero_kernel(const uint32_t* empty, uint32_t n, uint32
 
 }  // namespace
 
-#define KVF_GUARD(e)                                                                               \
-    if (!(e)) return set_error(KVF_E_INVALID_ARG, "null engine");                                  \
-    std::lock_guard<std::mutex> _lk((e)->mu);                                                      \
-    if (cudaSetDevice((e)->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed"); \
-    kvf_impl::clear_stale_error(e, __func__)
-
 extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
                                  const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale,
                                  void* out, uint32_t chunk_tokens) {
@@ -461,6 +455,8 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
         return set_error(KVF_E_INVALID_ARG, "chunk_tokens must be a multiple of 16 in [16, 2048] (0 = auto)");
     if (batch == 0) return KVF_OK;
     if (!q || !out || !run_counts) return set_error(KVF_E_INVALID_ARG, "null q / out / run_counts");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 3)
+        return set_error(KVF_E_INVALID_ARG, "q and out must be 4-byte aligned");
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
     const uint32_t hkv = e->geom.kv_heads_local, hq = hkv * group;
     const uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta));  // heads per CTA

@@ -685,12 +685,6 @@ uint32_t grid_for(const kvf_engine* e, uint64_t work, uint32_t threads) {
 // =====================================================================================
 // C-ABI
 // =====================================================================================
-#define KVF_GUARD(e) \
-    if (!(e)) return set_error(KVF_E_INVALID_ARG, "null engine"); \
-    std::lock_guard<std::mutex> _lk((e)->mu); \
-    if (cudaSetDevice((e)->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed"); \
-    kvf_impl::clear_stale_error(e, __func__)
-
 extern "C" {
 
 const char* kvf_last_error(void) { return g_last_error.c_str(); }

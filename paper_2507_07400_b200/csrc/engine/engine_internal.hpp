@@ -131,6 +131,14 @@ struct kvf_engine {
     std::mutex mu;  // engine calls are serialised per engine
 };
 
+// Entry of every engine C-ABI call: null check, the engine's mutex, its device, and any
+// non-sticky error another caller left pending taken out of the way.
+#define KVF_GUARD(e)                                                                                     \
+    if (!(e)) return kvf_impl::set_error(KVF_E_INVALID_ARG, "null engine");                              \
+    std::lock_guard<std::mutex> _lk((e)->mu);                                                            \
+    if (cudaSetDevice((e)->device) != cudaSuccess) return kvf_impl::set_error(KVF_E_CUDA, "cudaSetDevice failed"); \
+    kvf_impl::clear_stale_error(e, __func__)
+
 namespace kvf_impl {
 int acquire_event(kvf_engine* e, cudaEvent_t* ev);
 // a job = start event on `stream` ... kernels ... stop event (end_job registers it)

@@ -185,6 +185,8 @@ def test_attend_errors():
             e.attend(0, 17, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)   # group > 16
         with pytest.raises(N.KvfError):
             e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0, chunk=100)
+        with pytest.raises(N.KvfError):
+            e.attend(0, 4, q.data_ptr() + 2, [[(0, 10)]], out.data_ptr(), 1.0)   # misaligned q
     with Engine(layers=1, kv_heads_total=8, head_dim=64, gpu_slots=256, host_slots=0) as e:
         with pytest.raises(N.KvfError):
             e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)    # head_dim 128 only
