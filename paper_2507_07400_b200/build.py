@@ -64,7 +64,7 @@ def build_host(force=False):
 def build_oracle():
     _run(["make", "-C", os.path.join(ROOT, "oracle"), "liboracle.so"])
     if os.path.isdir("/root/reference/proj/src"):
-        _run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"])
+        _run(["make", "-C", os.path.join(ROOT, "oracle"), "ref", "suites"])
 
 
 def build_all(force=False):
