@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -25,6 +26,16 @@ RunList split_runs(RunList& runs, uint64_t tokens);
 
 // Maps an engine status onto the reference's ErrorCode convention (code = status - 1).
 [[noreturn]] void throw_engine(int status, const std::string& what);
+
+class Engine;
+
+// Drop-in for code written against the engine-less reference API (kvsim): a process-wide
+// factory that the RadixCache / TierManager / Simulator constructors ask for an engine when
+// none is passed (same bytes_per_token => the same engine, so a cache and a tier manager built
+// separately share it).  Unset -- the default -- nothing changes: no engine, no GPU path.
+using EngineFactory = std::function<Engine*(uint64_t bytes_per_token)>;
+void set_default_engine_factory(EngineFactory factory);
+Engine* default_engine(uint64_t bytes_per_token);  // nullptr when no factory is installed
 
 struct EngineOptions {
     uint32_t layers = 32, kv_heads_total = 8, kv_heads_local = 8, head_offset = 0, head_dim = 128;

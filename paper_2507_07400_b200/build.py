@@ -65,6 +65,8 @@ def build_oracle():
     _run(["make", "-C", os.path.join(ROOT, "oracle"), "liboracle.so"])
     if os.path.isdir("/root/reference/proj/src"):
         _run(["make", "-C", os.path.join(ROOT, "oracle"), "ref", "suites"])
+        # the reference's own unit suites against OUR host API (tests/refsuite/README.md)
+        _run(["make", "-C", os.path.join(ROOT, "tests", "refsuite")])
 
 
 def build_all(force=False):

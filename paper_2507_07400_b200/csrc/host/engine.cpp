@@ -4,6 +4,7 @@
 #include "kvflow/engine.hpp"
 
 #include <algorithm>
+#include <mutex>
 
 namespace kvf {
 
@@ -40,6 +41,21 @@ void throw_engine(int status, const std::string& what) {
         int _rc = (expr);                       \
         if (_rc != KVF_OK) throw_engine(_rc, #expr); \
     } while (0)
+
+namespace {
+std::mutex g_factory_mu;
+EngineFactory g_factory;
+}  // namespace
+
+void set_default_engine_factory(EngineFactory factory) {
+    std::lock_guard<std::mutex> lk(g_factory_mu);
+    g_factory = std::move(factory);
+}
+
+Engine* default_engine(uint64_t bytes_per_token) {
+    std::lock_guard<std::mutex> lk(g_factory_mu);
+    return g_factory ? g_factory(bytes_per_token) : nullptr;
+}
 
 Engine::Engine(const EngineOptions& opt) : opt_(opt) {
     kvf_geometry g{opt.layers, opt.kv_heads_total, opt.kv_heads_local, opt.head_offset, opt.head_dim, 2};

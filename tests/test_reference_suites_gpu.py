@@ -1,0 +1,35 @@
+"""The reference's OWN unit suites run against the B200 host API (tests/refsuite/).
+
+proj/tests/test_*.cpp (55 doctest cases, the reference authors' known-answer tests for the
+radix cache, tier manager, scheduler, step graph, cost model and workload generator) compile
+UNMODIFIED against include/kvflow through a kvsim -> kvflow include shim; the default-engine
+factory (kvf::set_default_engine_factory) puts every RadixCache / TierManager / Simulator
+they build on a GPU engine, so their evictions and priorities run as K4/K5 and their
+transfers as K1/K2.  The result must equal the reference's own run of the same suites
+(tests/test_reference_suites.py): 52 cases pass and the reference's three known failures
+ fail at the same lines.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "refsuite", "_bin")
+SUITES = ["cost_model", "radix_cache", "scheduler", "step_graph", "tier_manager", "workload"]
+KNOWN = {"test_scheduler.cpp:310", "test_scheduler.cpp:313", "test_scheduler.cpp:345", "test_scheduler.cpp:418"}
+
+
+@pytest.mark.skipif(not all(os.path.exists(os.path.join(BIN, f"suite_{s}")) for s in SUITES),
+                    reason="tests/refsuite not built (needs /root/reference at build time)")
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_the_gpu_engine(suite):
+    r = subprocess.run([os.path.join(BIN, f"suite_{suite}")], capture_output=True, text=True, timeout=600)
+    fails = {f"{os.path.basename(m.group(1))}:{m.group(2)}" for m in re.finditer(r"^FAIL (\S+):(\d+):", r.stdout, re.M)}
+    expected = {k for k in KNOWN if k.startswith(f"test_{suite}.cpp")}
+    assert fails == expected, r.stdout[-3000:]
+    m = re.search(r"test cases: (\d+) \| (\d+) passed", r.stdout)
+    assert m and int(m.group(1)) - int(m.group(2)) == (3 if suite == "scheduler" else 0), r.stdout[-2000:]
