@@ -14,6 +14,7 @@
  *   kvf_priority_propagate<- RadixCache::set_agent_priorities proj/src/radix_cache.cpp:266-285 [K4]
  *   kvf_victim_select     <- RadixCache::evict (selection) proj/src/radix_cache.cpp:302-372 [K5]
  *   kvf_decode_attend     <- (new) decode-side consumer of the slot-run table, SURVEY §8f-3 [K6]
+ *   kvf_peer_gather       <- (new) NVLink fetch from a replica's HBM, SURVEY §8f-4
  *   kvf_slots_alloc/free  <- (new) token-slot pools; the reference keeps only a byte ledger
  *                            (GpuPool, proj/include/kvsim/tier_manager.hpp:38-46)
  *
@@ -135,6 +136,16 @@ int kvf_d2h_scatter(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uin
 int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* dev_runs, uint32_t n_dev, void* staging);
 int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* dev_runs,
                     uint32_t n_dev);
+
+/* Peer fetch (SURVEY §8f-4 follow-on): copy a node's KV from ANOTHER engine's HBM pool --
+ * typically a data-parallel replica on another GPU of the box, read over NVLink / NVSwitch by
+ * a K3-style kernel on this GPU -- instead of reloading it from host memory over PCIe.
+ * Both engines must hold the same shard geometry; src == e copies within one pool.  The
+ * caller guarantees the source node is resident (its load, if any, has completed) and not
+ * released while the job runs; the source engine's own payload writes are waited for.
+ * Async on this engine's HBM stream as job `job_id`. */
+int kvf_peer_gather(kvf_engine* e, uint64_t job_id, kvf_engine* src, const kvf_run* src_runs, uint32_t n_src,
+                    const kvf_run* dst_runs, uint32_t n_dst);
 
 /* K2 for several nodes in ONE launch (small-node write-back batching):
  * job k moves dev_runs[off_k .. off_k + dev_counts[k]) -> host_runs[...host_counts[k]), the

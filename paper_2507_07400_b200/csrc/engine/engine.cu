@@ -1077,6 +1077,49 @@ int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const k
     return dev_staging_copy(e, job_id, runs, n, static_cast<char*>(const_cast<void*>(staging)), false);
 }
 
+int kvf_peer_gather(kvf_engine* e, uint64_t job_id, kvf_engine* src, const kvf_run* src_runs, uint32_t n_src,
+                    const kvf_run* dst_runs, uint32_t n_dst) {
+    if (!e || !src) return set_error(KVF_E_INVALID_ARG, "null engine");
+    // both pools are touched: hold both engines (std::lock takes the pair deadlock-free)
+    std::unique_lock<std::mutex> l1(e->mu, std::defer_lock), l2(src->mu, std::defer_lock);
+    if (src == e) l1.lock();
+    else std::lock(l1, l2);
+    if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
+    kvf_impl::clear_stale_error(e, __func__);
+    if (e->tpb != src->tpb || e->planes != src->planes || e->geom.head_offset != src->geom.head_offset)
+        return set_error(KVF_E_INVALID_ARG, "peer engine holds a different KV shard geometry");
+    uint64_t ts = 0, td = 0;
+    if ((n_src && !src_runs) || (n_dst && !dst_runs)) return set_error(KVF_E_INVALID_ARG, "null run list");
+    if (!runs_valid(src, KVF_TIER_DEVICE, src_runs, n_src, &ts) || !runs_valid(e, KVF_TIER_DEVICE, dst_runs, n_dst, &td))
+        return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    if (ts != td) return set_error(KVF_E_INVALID_ARG, "source and destination token counts differ");
+    if (src->device != e->device) {  // NVLink / NVSwitch: the kernel on this GPU loads the peer's HBM
+        int can = 0;
+        KVF_CUDA(cudaDeviceCanAccessPeer(&can, e->device, src->device));
+        if (!can) return set_error(KVF_E_INVALID_ARG, "no peer access between the two GPUs");
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(src->device, 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (pe != cudaSuccess) return cuda_error(pe, "cudaDeviceEnablePeerAccess");
+    }
+    std::vector<Piece> pieces;
+    merge_runs(src_runs, n_src, dst_runs, n_dst, pieces);
+    Job j;
+    int rc = begin_job(e, job_id, e->s_dev, j);
+    if (rc) return rc;
+    // the source's own payload writes (fills, K3 scatters) must have landed
+    if (src != e && src->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_dev, src->dev_write_done, 0));
+    Endpoint from{src->dev_pool, src->dev_slots * src->tpb, false};
+    Endpoint to{e->dev_pool, e->dev_slots * e->tpb, false};
+    rc = launch_copy(e, e->s_dev, from, to, pieces, KVF_COPY_SM_VEC, e->cfg.hbm_ctas);
+    if (rc) return rc;
+    KVF_CUDA(cudaEventRecord(e->dev_write_done, e->s_dev));  // new bytes in this pool
+    e->dev_write_pending = true;
+    j.bytes = ts * e->token_bytes;
+    e->stats.dev_bytes += j.bytes;
+    e->stats.dev_jobs++;
+    return end_job(e, job_id, j);
+}
+
 int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done) {
     KVF_GUARD(e);
     auto it = e->jobs.find(job_id);

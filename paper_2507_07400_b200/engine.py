@@ -153,6 +153,13 @@ class Engine:
         N.check(self._lib.kvf_job_span_ms(self.h, first_job, last_job, C.byref(ms)))
         return ms.value
 
+    def peer_gather(self, src, src_runs, dst_runs, job=None):
+        """Copy a node from another engine's HBM pool (NVLink on another GPU) into dst_runs."""
+        job = job or self.new_job()
+        N.check(self._lib.kvf_peer_gather(self.h, job, src.h, N.runs_array(src_runs), len(src_runs),
+                                          N.runs_array(dst_runs), len(dst_runs)))
+        return job
+
     def dev_gather(self, dev_runs, staging_ptr, job=None):
         job = job or self.new_job()
         N.check(self._lib.kvf_dev_gather(self.h, job, N.runs_array(dev_runs), len(dev_runs), staging_ptr))
