@@ -14,6 +14,7 @@
  *   kvf_priority_propagate<- RadixCache::set_agent_priorities proj/src/radix_cache.cpp:266-285 [K4]
  *   kvf_victim_select     <- RadixCache::evict (selection) proj/src/radix_cache.cpp:302-372 [K5]
  *   kvf_decode_attend     <- (new) decode-side consumer of the slot-run table, SURVEY §8f-3 [K6]
+ *   kvf_kv_append         <- (new) its write side: a layer's new K/V rows into slot runs
  *   kvf_peer_gather       <- (new) NVLink fetch from a replica's HBM, SURVEY §8f-4
  *   kvf_slots_alloc/free  <- (new) token-slot pools; the reference keeps only a byte ledger
  *                            (GpuPool, proj/include/kvsim/tier_manager.hpp:38-46)
@@ -224,6 +225,15 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_
                       uint8_t* out_action, uint32_t* out_count, uint64_t* out_immediate, uint64_t* out_pending);
 
 /* ---- decode-side consumer of the slot-run table ------------------------ */
+/* KV write side of the same layout: store freshly computed K and V of `ntok` tokens for one
+ * layer (a prefill chunk, or one decode token per sequence) into HBM slot runs.
+ *   k, v: device bf16 [ntok][kv_heads_local][head_dim] -- the model's projection layout;
+ *   runs: the tokens' slots in order (sum of lengths == ntok).
+ * Async on the engine's payload-write stream as job `job_id`; write-backs (K2) and K6 calls
+ * issued later are ordered after it.  k / v must be ready when the call is made. */
+int kvf_kv_append(kvf_engine* e, uint64_t job_id, uint32_t layer, const kvf_run* runs, uint32_t n_runs, const void* k,
+                  const void* v, uint64_t ntok);
+
 /* K6: one decode step of GQA attention, reading layer `layer`'s K and V IN PLACE from the
  * HBM pool through each sequence's slot-run list (what RadixCache::match_prefix hands out,
  * proj/src/radix_cache.cpp:88-140, plus the request's suffix) -- no compaction copy.

@@ -85,6 +85,8 @@ _ENGINE_SIGS = {
     "kvf_d2h_scatter": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.POINTER(Run), C.c_uint32]),
     "kvf_d2h_scatter_batch": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64), C.POINTER(Run),
                                         C.POINTER(C.c_uint32), C.POINTER(Run), C.POINTER(C.c_uint32)]),
+    "kvf_kv_append": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(Run), C.c_uint32, C.c_void_p,
+                                C.c_void_p, C.c_uint64]),
     "kvf_peer_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(Run), C.c_uint32, C.POINTER(Run),
                                   C.c_uint32]),
     "kvf_dev_gather": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(Run), C.c_uint32, C.c_void_p]),

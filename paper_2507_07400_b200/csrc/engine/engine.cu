@@ -524,7 +524,8 @@ struct Endpoint {
 // Launch the copy of `pieces` (all planes) between two pools on `stream`.
 int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const Endpoint& dst,
                 const std::vector<Piece>& pieces, uint32_t mode, uint32_t ctas, uint32_t* layer_ready = nullptr,
-                uint64_t* tiles_per_layer = nullptr) {
+                uint64_t* tiles_per_layer = nullptr, uint32_t planes = 0) {
+    if (planes == 0) planes = e->planes;  // default: every plane of the token (a whole node)
     if (layer_ready) mode = KVF_COPY_SM_VEC;  // only the vector kernel publishes per-layer progress
     const uint64_t tpb = e->tpb;
     for (size_t first = 0; first < pieces.size(); first += kMaxPieces) {
@@ -533,7 +534,7 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
             for (uint32_t i = 0; i < np; ++i) {
                 const Piece& pc = pieces[first + i];
                 KVF_CUDA(cudaMemcpy2DAsync(const_cast<char*>(dst.base) + pc.dst_slot * tpb, dst.stride,
-                                           src.base + pc.src_slot * tpb, src.stride, pc.ntok * tpb, e->planes,
+                                           src.base + pc.src_slot * tpb, src.stride, pc.ntok * tpb, planes,
                                            cudaMemcpyDefault, stream));
             }
             continue;
@@ -544,7 +545,7 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         p.dst = const_cast<char*>(dst.base);
         p.src_stride = src.stride;
         p.dst_stride = dst.stride;
-        p.planes = e->planes;
+        p.planes = planes;
         p.npieces = np;
         const bool vec16 = (tpb % 16) == 0;
         // PCIe jobs keep ~the link's bandwidth-delay product in flight (8 CTAs x 256 thr x 4 x
@@ -556,7 +557,7 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         // 64 KiB (4 batches of 256 x 4 x 16 B), HBM tiles 64 KiB (one batch of 512 x 8 x 16 B)
         p.tile_bytes = threads * unroll * (vec16 ? 16 : 8) * (pcie ? 4 : 1);
         uint64_t tiles = 0;
-        const uint64_t per_piece_planes = layer_ready ? 1 : e->planes;
+        const uint64_t per_piece_planes = layer_ready ? 1 : planes;
         for (uint32_t i = 0; i < np; ++i) {
             const Piece& pc = pieces[first + i];
             p.src_off[i] = pc.src_slot * tpb;
@@ -571,7 +572,7 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
             p.plane_tiles = tiles;
             p.layer_ready = layer_ready;
             if (tiles_per_layer) *tiles_per_layer += 2 * tiles;
-            tiles *= e->planes;
+            tiles *= planes;
         }
         p.total_tiles = tiles;
         if (tiles == 0) continue;
@@ -1075,6 +1076,37 @@ int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* runs, uint32_t
 int kvf_dev_scatter(kvf_engine* e, uint64_t job_id, const void* staging, const kvf_run* runs, uint32_t n) {
     KVF_GUARD(e);
     return dev_staging_copy(e, job_id, runs, n, static_cast<char*>(const_cast<void*>(staging)), false);
+}
+
+int kvf_kv_append(kvf_engine* e, uint64_t job_id, uint32_t layer, const kvf_run* runs, uint32_t n_runs, const void* k,
+                  const void* v, uint64_t ntok) {
+    KVF_GUARD(e);
+    if (layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "layer out of range");
+    if (ntok && (!k || !v)) return set_error(KVF_E_INVALID_ARG, "null k / v");
+    uint64_t td = 0;
+    if (n_runs && !runs) return set_error(KVF_E_INVALID_ARG, "null run list");
+    if (!runs_valid(e, KVF_TIER_DEVICE, runs, n_runs, &td)) return set_error(KVF_E_INVALID_ARG, "run out of pool range");
+    if (td != ntok) return set_error(KVF_E_INVALID_ARG, "runs and ntok disagree");
+    const kvf_run whole{0, ntok};
+    std::vector<Piece> pieces;
+    merge_runs(&whole, 1, runs, n_runs, pieces);
+    Job j;
+    int rc = begin_job(e, job_id, e->s_dev, j);  // the payload-write stream: later K2 / K6 order after it
+    if (rc) return rc;
+    const uint64_t plane = e->dev_slots * e->tpb;
+    char* kplane = e->dev_pool + static_cast<uint64_t>(2 * layer) * plane;
+    for (int kv = 0; kv < 2; ++kv) {  // [ntok][heads][dim] rows -> the layer's K / V plane rows
+        Endpoint from{static_cast<const char*>(kv ? v : k), ntok * e->tpb, false};
+        Endpoint to{kplane + kv * plane, plane, false};
+        rc = launch_copy(e, e->s_dev, from, to, pieces, KVF_COPY_SM_VEC, e->cfg.hbm_ctas, nullptr, nullptr, 1);
+        if (rc) return rc;
+    }
+    KVF_CUDA(cudaEventRecord(e->dev_write_done, e->s_dev));
+    e->dev_write_pending = true;
+    j.bytes = 2 * ntok * e->tpb;
+    e->stats.dev_bytes += j.bytes;
+    e->stats.dev_jobs++;
+    return end_job(e, job_id, j);
 }
 
 int kvf_peer_gather(kvf_engine* e, uint64_t job_id, kvf_engine* src, const kvf_run* src_runs, uint32_t n_src,

@@ -153,6 +153,12 @@ class Engine:
         N.check(self._lib.kvf_job_span_ms(self.h, first_job, last_job, C.byref(ms)))
         return ms.value
 
+    def kv_append(self, layer, runs, k_ptr, v_ptr, ntok, job=None):
+        """Write a layer's new K/V rows (device bf16 [ntok][kv_heads_local][128]) into slot runs."""
+        job = job or self.new_job()
+        N.check(self._lib.kvf_kv_append(self.h, job, layer, N.runs_array(runs), len(runs), k_ptr, v_ptr, ntok))
+        return job
+
     def peer_gather(self, src, src_runs, dst_runs, job=None):
         """Copy a node from another engine's HBM pool (NVLink on another GPU) into dst_runs."""
         job = job or self.new_job()

@@ -190,3 +190,44 @@ def test_attend_errors():
     with Engine(layers=1, kv_heads_total=8, head_dim=64, gpu_slots=256, host_slots=0) as e:
         with pytest.raises(N.KvfError):
             e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)    # head_dim 128 only
+
+
+@pytest.mark.parametrize("kv_local", [8, 2])
+def test_append_then_decode_attend(kv_local):
+    """kvf_kv_append writes a layer's K/V rows ([ntok][heads][128], the model's layout) into
+    fragmented slot runs bit-exactly; a decode step then appends one token per sequence and
+    K6 attends over prefix + new token straight from the pool."""
+    need_gpu()
+    rng = np.random.default_rng(21 + kv_local)
+    layers, lens = 2, [500, 37]
+    with Engine(layers=layers, kv_heads_total=8, kv_heads_local=kv_local, head_offset=8 - kv_local,
+                gpu_slots=4096, host_slots=0) as e:
+        seqs, kv = [], []
+        for n in lens:  # prefill: every layer's K and V appended into fragmented runs
+            runs = fragmented_runs(e, n, rng, 60)
+            t = torch.randn(layers, 2, n, kv_local, 128, device="cuda").to(torch.bfloat16)
+            torch.cuda.synchronize()
+            for l in range(layers):
+                j = e.kv_append(l, runs, t[l, 0].data_ptr(), t[l, 1].data_ptr(), n)
+                e.wait(j)
+                e.release(j)
+            got = torch.from_numpy(e.read(N.KVF_TIER_DEVICE, runs).view(np.int16)).view(2 * layers, n, kv_local, 128)
+            assert torch.equal(got, t.reshape(2 * layers, n, kv_local, 128).view(torch.int16).cpu()), "bytes differ"
+            seqs.append(runs)
+            kv.append(t)
+        # decode step: one new token per sequence, appended per layer, then attended
+        new = [e.alloc(N.KVF_TIER_DEVICE, 1) for _ in lens]
+        tn = torch.randn(len(lens), layers, 2, 1, kv_local, 128, device="cuda").to(torch.bfloat16)
+        q = torch.randn(len(lens), kv_local * 4, 128, device="cuda").to(torch.bfloat16)
+        out = torch.empty_like(q)
+        torch.cuda.synchronize()
+        for l in range(layers):
+            for b in range(len(lens)):
+                j = e.kv_append(l, new[b], tn[b, l, 0].data_ptr(), tn[b, l, 1].data_ptr(), 1)
+                e.release(j)
+            ja = e.attend(l, 4, q.data_ptr(), [seqs[b] + new[b] for b in range(len(lens))], out.data_ptr(), 0.09)
+            e.wait(ja)
+            e.release(ja)
+            full = [torch.cat([kv[b], tn[b]], dim=2).reshape(2 * layers, lens[b] + 1, kv_local, 128)
+                    for b in range(len(lens))]
+            check(out, reference(q, full, l, 4, 0.09))
