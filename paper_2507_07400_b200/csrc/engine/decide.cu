@@ -533,9 +533,13 @@ int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
 int spin_decision(kvf_engine* e, const unsigned long long* hdr, unsigned long long seq,
                   std::chrono::steady_clock::time_point t0) {
     const volatile unsigned long long* flag = hdr + kDoneWord;
+    // a faulted kernel never publishes: look at the stream only after 200 us, then every 100 us
+    // (a driver call inside the normal ~10-30 us wait would only delay seeing the done word)
+    auto next_check = t0 + std::chrono::microseconds(200);
     for (uint32_t it = 1;; ++it) {
         if (__atomic_load_n(const_cast<const unsigned long long*>(flag), __ATOMIC_ACQUIRE) == seq) break;
-        if ((it & 255) == 0) {
+        if ((it & 63) == 0 && std::chrono::steady_clock::now() >= next_check) {
+            next_check = std::chrono::steady_clock::now() + std::chrono::microseconds(100);
             const cudaError_t st = cudaStreamQuery(e->s_dec);
             if (st != cudaSuccess && st != cudaErrorNotReady) return cuda_error(st, "decision kernel");
             if (st == cudaSuccess && __atomic_load_n(const_cast<const unsigned long long*>(flag), __ATOMIC_ACQUIRE) != seq)
