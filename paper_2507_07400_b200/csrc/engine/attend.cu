@@ -389,27 +389,54 @@ __global__ void __launch_bounds__(kCombWarps * 32) kvf_attend_combine_kernel(con
     if (n <= 1) return;  // written by the main kernel (or an empty sequence)
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, head = hq / group, row = hq % group;
     auto key = [&](uint32_t i) { return (static_cast<uint64_t>(i0 + i) * hkv + head) * group + row; };
-    float M = -INFINITY;
-    for (uint32_t i = tid; i < n; i += kCombWarps * 32) M = fmaxf(M, part_ml[key(i) * 2]);
+    // every warp pulls its first kRegs partials into registers at once (independent loads),
+    // one block-wide max, then rescales from registers; partials beyond 8 x kRegs (a very long
+    // sequence) take a second, load-then-scale pass
+    constexpr int kRegs = 8;
+    float2 ml[kRegs];
+    float4 ov[kRegs];
+    float mloc = -INFINITY;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    if (lane == 0) red_x[warp] = M;
+    for (int k = 0; k < kRegs; ++k) {
+        const uint32_t i = warp + k * kCombWarps;
+        ml[k] = make_float2(-INFINITY, 0.f);
+        ov[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < n) {
+            const uint64_t kk = key(i);
+            ml[k] = *reinterpret_cast<const float2*>(part_ml + kk * 2);
+            ov[k] = reinterpret_cast<const float4*>(part_o + kk * kD)[lane];
+        }
+        mloc = fmaxf(mloc, ml[k].x);
+    }
+    for (uint32_t i = warp + kRegs * kCombWarps; i < n; i += kCombWarps)
+        mloc = fmaxf(mloc, part_ml[key(i) * 2]);
+    if (lane == 0) red_x[warp] = mloc;
     __syncthreads();
+    float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kCombWarps; ++w) M = fmaxf(M, red_x[w]);
     float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
     float l = 0.f;
+#pragma unroll
+    for (int k = 0; k < kRegs; ++k) {
+        const float sc = ml[k].x == -INFINITY ? 0.f : exp2f(ml[k].x - M);
+        o.x += sc * ov[k].x;
+        o.y += sc * ov[k].y;
+        o.z += sc * ov[k].z;
+        o.w += sc * ov[k].w;
+        l += sc * ml[k].y;
+    }
 #pragma unroll 4
-    for (uint32_t i = warp; i < n; i += kCombWarps) {
+    for (uint32_t i = warp + kRegs * kCombWarps; i < n; i += kCombWarps) {
         const uint64_t k = key(i);
-        const float2 ml = *reinterpret_cast<const float2*>(part_ml + k * 2);
-        const float sc = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
+        const float2 m2 = *reinterpret_cast<const float2*>(part_ml + k * 2);
+        const float sc = m2.x == -INFINITY ? 0.f : exp2f(m2.x - M);
         const float4 v = reinterpret_cast<const float4*>(part_o + k * kD)[lane];
         o.x += sc * v.x;
         o.y += sc * v.y;
         o.z += sc * v.z;
         o.w += sc * v.w;
-        l += sc * ml.y;
+        l += sc * m2.y;
     }
     red_o[warp][lane] = o;
     if (lane == 0) red_l[warp] = l;
