@@ -63,9 +63,11 @@ static_assert(kWarps * kWarpRing >= kWarps * 16 * kRedStride * 4 + 2 * kWarps * 
 
 struct AttnItem {
     uint32_t seq, t0, ntok, r0, nr;
-    uint32_t nsib;  // items of this sequence (1: the CTA writes the output itself)
-    uint32_t pad0, pad1;  // 32 B
+    uint32_t nsib;   // items of this sequence (1: the CTA writes the output itself)
+    uint32_t slot0;  // nr == 1: slot of the item's first token (its slots are slot0, slot0 + 1, ...)
+    uint32_t pad;    // 32 B
 };
+constexpr uint32_t kParamItems = 160;  // items that ride in the launch parameters (5 KiB: one wave)
 
 struct AttnParams {
     const char* pool;        // HBM pool base
@@ -83,6 +85,8 @@ struct AttnParams {
     float* part_o;             // [items][hkv][group][128]
     float* part_ml;            // [items][hkv][group][2]
     unsigned long long* trace; // diagnostics (KVF_ATTEND_TRACE): per CTA start, prologue, loop, end, smid
+    uint32_t inline_items;     // 1: items[] below (grid <= kParamItems), else p.items in global memory
+    AttnItem items_p[kParamItems];
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned long long t_start = p.trace ? gtime() : 0;
-    const AttnItem it = p.items[blockIdx.x];
+    // the item comes with the launch (parameter space) unless the grid is very large
+    const AttnItem it = p.inline_items ? p.items_p[blockIdx.x] : p.items[blockIdx.x];
     // warp -> (head, sub-stream): the CTA's hpc heads x (8 / hpc) interleaved tile streams
     const uint32_t hl = warp % p.hpc, sub = warp / p.hpc, nsub = kWarps / p.hpc;
     const uint32_t head = blockIdx.y * p.hpc + hl;
@@ -153,22 +158,27 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
         qa[kk][3] = g + 8 < p.group ? *reinterpret_cast<const uint32_t*>(qb + (g + 8) * kD + d0 + 8) : 0u;
     }
 
-    // ---- token -> slot map of the item (runs cached in smem, one binary search per token)
-    for (uint32_t r = tid; r < it.nr; r += kThreads) {
-        rtok_s[r] = p.run_tok[it.r0 + r];
-        rslot_s[r] = p.run_slot[it.r0 + r];
-    }
-    __syncthreads();
-    for (uint32_t j = tid; j < it.ntok; j += kThreads) {
-        const uint32_t t = it.t0 + j;
-        uint32_t lo = 0, hi = it.nr - 1;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi + 1) >> 1;
-            if (rtok_s[mid] <= t) lo = mid; else hi = mid - 1;
+    // ---- token -> slot map.  An item inside one run (the common case: runs are long) addresses
+    // slot0 + j directly and its first loads leave at once; otherwise the runs are cached in smem
+    // and every token's slot is found by binary search
+    const bool one_run = it.nr == 1;
+    if (!one_run) {
+        for (uint32_t r = tid; r < it.nr; r += kThreads) {
+            rtok_s[r] = p.run_tok[it.r0 + r];
+            rslot_s[r] = p.run_slot[it.r0 + r];
         }
-        slot_s[j] = rslot_s[lo] + (t - rtok_s[lo]);
+        __syncthreads();
+        for (uint32_t j = tid; j < it.ntok; j += kThreads) {
+            const uint32_t t = it.t0 + j;
+            uint32_t lo = 0, hi = it.nr - 1;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi + 1) >> 1;
+                if (rtok_s[mid] <= t) lo = mid; else hi = mid - 1;
+            }
+            slot_s[j] = rslot_s[lo] + (t - rtok_s[lo]);
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
     const unsigned long long t_pro = p.trace ? gtime() : 0;
     // ---- per-warp pipeline over tiles sub, sub + nsub, ... of the item, for its head
@@ -187,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
         for (int k = 0; k < kTok / 2; ++k) {
             const uint32_t r = lr + 2 * k, j = tb + r;
             const bool ok = j < it.ntok;
-            const uint64_t off = static_cast<uint64_t>(slot_s[ok ? j : 0]) * p.tpb + lc * 16;
+            const uint32_t slot = one_run ? it.slot0 + (ok ? j : 0) : slot_s[ok ? j : 0];
+            const uint64_t off = static_cast<uint64_t>(slot) * p.tpb + lc * 16;
             cp_async16(smem_u32(kb + swz(r, lc)), kplane + off, ok);
             cp_async16(smem_u32(vb + swz(r, lc)), vplane + off, ok);
         }
@@ -586,7 +597,8 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
                 if (r + kMaxRuns < rend) end = std::min<uint64_t>(end, rtok[r + kMaxRuns]);
                 uint32_t nr = 0;
                 while (r + nr < rend && rtok[r + nr] < end) ++nr;
-                items.push_back(AttnItem{b, static_cast<uint32_t>(t), static_cast<uint32_t>(end - t), r, nr, 0, 0, 0});
+                items.push_back(AttnItem{b, static_cast<uint32_t>(t), static_cast<uint32_t>(end - t), r, nr, 0,
+                                         rslot[r] + static_cast<uint32_t>(t - rtok[r]), 0});
                 t = end;
             }
             for (size_t i = first; i < items.size(); ++i) items[i].nsib = static_cast<uint32_t>(items.size() - first);
@@ -614,6 +626,8 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
         if (e->att_upload_pending) KVF_CUDA(cudaEventSynchronize(e->att_upload_done));
         char* hs = static_cast<char*>(e->ws_att.host);
         std::memcpy(hs, items.data(), nitems * sizeof(AttnItem));
+        e->att_items.assign(reinterpret_cast<const uint8_t*>(items.data()),
+                            reinterpret_cast<const uint8_t*>(items.data() + nitems));
         std::memcpy(hs + b_items, rtok.data(), nruns * 4);
         std::memcpy(hs + b_items + b_rt, rslot.data(), nruns * 4);
         std::memcpy(hs + b_items + b_rt + b_rs, seq_item0.data(), (batch + 1) * 4);
@@ -650,6 +664,10 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
     prm.q = static_cast<const __nv_bfloat16*>(q);
     prm.out = static_cast<__nv_bfloat16*>(out);
     prm.items = reinterpret_cast<const AttnItem*>(ds);
+    if (nitems <= kParamItems) {  // one wave: the items travel with the launch
+        prm.inline_items = 1;
+        std::memcpy(prm.items_p, e->att_items.data(), nitems * sizeof(AttnItem));
+    }
     prm.run_tok = reinterpret_cast<const uint32_t*>(ds + b_items);
     prm.run_slot = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt);
     const uint32_t* d_seq_item0 = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt + b_rs);

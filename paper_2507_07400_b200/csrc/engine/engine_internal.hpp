@@ -118,6 +118,7 @@ struct kvf_engine {
     bool att_upload_pending = false, attend_attr_set = false;
     int attend_occ = 0;  // resident K6 CTAs per SM
     std::vector<uint64_t> att_sig;  // K6 descriptor cache: inputs of the blob now in ws_att.dev
+    std::vector<uint8_t> att_items;  // K6 work items of that blob (host copy for the launch parameters)
     uint64_t att_meta[10] = {};     //   and its sizes (a decode step calls K6 once per layer)
     kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
     std::map<uint64_t, kvf_impl::BigGraph> big_graphs;  // key: bucket << 1 | workflow_aware
