@@ -10,7 +10,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2507_07400_b200 import sim as S  # noqa: E402
 
-CONFIGS = {"C1": dict(fixed=2048, gpu_cap=855638016), "C2": dict(fixed=8192, gpu_cap=3271557120)}
+CONFIGS = {"C1": dict(fixed=2048, gpu_cap=855638016), "C2": dict(fixed=8192, gpu_cap=3271557120),
+           # the paper's flagship shape (10 agents, 8192/32/32, 1.83x vs HiCache on A10G),
+           # here on B200 PCIe with h100-qwen32b compute; budget 3.0 agent footprints
+           "P10": dict(agents=10, iterations=4, fixed=8192, dyn=32, out=32, gpu_cap=3 * (8192 + 64) * 131072)}
 
 
 def one(policy, cfg, **kw):
