@@ -13,7 +13,11 @@ from paper_2507_07400_b200 import sim as S  # noqa: E402
 CONFIGS = {"C1": dict(fixed=2048, gpu_cap=855638016), "C2": dict(fixed=8192, gpu_cap=3271557120),
            # the paper's flagship shape (10 agents, 8192/32/32, 1.83x vs HiCache on A10G),
            # here on B200 PCIe with h100-qwen32b compute; budget 3.0 agent footprints
-           "P10": dict(agents=10, iterations=4, fixed=8192, dyn=32, out=32, gpu_cap=3 * (8192 + 64) * 131072)}
+           "P10": dict(agents=10, iterations=4, fixed=8192, dyn=32, out=32, gpu_cap=3 * (8192 + 64) * 131072),
+           # C4, the paper's concurrency regime (64 workflows, 1024-token fixed
+           # prompts), as one 8-way KV-head shard of Llama-3-8B (16 KiB/token, 2 GiB budget)
+           "C4s": dict(workflows=64, agents=4, iterations=4, fixed=1024, shared_prefix=512, dyn=256, out=256,
+                       bytes_per_token=16384, gpu_cap=2 * 1024**3)}
 
 
 def one(policy, cfg, **kw):
@@ -41,12 +45,17 @@ def one(policy, cfg, **kw):
 
 def main():
     out = {}
+    only = sys.argv[1:]  # optional config names
     for name, cfg in CONFIGS.items():
+        if only and name not in only:
+            continue
         for pol in ("LRU_GPU_ONLY", "LRU_REACTIVE_HICACHE", "KVFLOW"):
             out[f"{name}/{pol}"] = one(pol, cfg)
         out[f"{name}/KVFLOW+retry"] = one("KVFLOW", cfg, prefetch_retry=1)
         out[f"{name}/LRU_REACTIVE_HICACHE+layered"] = one("LRU_REACTIVE_HICACHE", cfg, layered_gate=1)
     for name in CONFIGS:
+        if f"{name}/KVFLOW" not in out:
+            continue
         k = out[f"{name}/KVFLOW"]["step_latency_mean_s"]
         out[f"{name}/speedup_vs_hicache"] = round(out[f"{name}/LRU_REACTIVE_HICACHE"]["step_latency_mean_s"] / k, 3)
         out[f"{name}/speedup_vs_gpu_only"] = round(out[f"{name}/LRU_GPU_ONLY"]["step_latency_mean_s"] / k, 3)
