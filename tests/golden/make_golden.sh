@@ -50,4 +50,8 @@ done
 # tests/cpp/c3_harness.hpp); one Llama-3-8B KV head (16 KiB/token), 24k-token budget
 "$ROOT/oracle/_ref/ref_c3" 3 4 16384 393216000 > "$G/c3_seed3.jsonl"
 "$ROOT/oracle/_ref/ref_c3" 11 6 16384 262144000 > "$G/c3_seed11.jsonl"
+for c in "5 4 327680000" "7 5 294912000" "13 4 360448000" "17 6 425984000" "19 3 229376000" "23 5 491520000"; do
+  set -- $c
+  "$ROOT/oracle/_ref/ref_c3" "$1" "$2" 16384 "$3" > "$G/c3_seed$1.jsonl"
+done
 echo "golden fixtures regenerated in $G"

@@ -28,8 +28,11 @@ def _build():
     return exe
 
 
-@pytest.mark.parametrize("fixture,args", [("c3_seed3.jsonl", ["3", "4", "16384", "393216000"]),
-                                          ("c3_seed11.jsonl", ["11", "6", "16384", "262144000"])])
+C3_CASES = [("3", "4", "393216000"), ("11", "6", "262144000"), ("5", "4", "327680000"), ("7", "5", "294912000"),
+            ("13", "4", "360448000"), ("17", "6", "425984000"), ("19", "3", "229376000"), ("23", "5", "491520000")]
+
+
+@pytest.mark.parametrize("fixture,args", [(f"c3_seed{s}.jsonl", [s, it, "16384", cap]) for s, it, cap in C3_CASES])
 def test_c3_matches_reference(fixture, args):
     exe = _build()
     r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600)
