@@ -48,10 +48,14 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line).  The sampler
+    starts before the region and waits for its first row (nvidia-smi needs ~0.1-0.3 s to come
+    up, as long as the whole timed region); every row is timestamped on arrival and the summary
+    keeps the rows inside [mark_start, mark_end] -- the nearest row when none fell inside."""
 
     def __init__(self, device):
         self.device, self.rows, self._p = device, [], None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -59,15 +63,27 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, text=True)
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            deadline = time.perf_counter() + 3.0
+            while not self.rows and time.perf_counter() < deadline:
+                time.sleep(0.01)
         except OSError:
             self._p = None
         return self
 
     def _read(self):
         for line in self._p.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
+        deadline = self.t1 + 0.2  # let the row covering the end of the region arrive
+        while time.perf_counter() < deadline and not any(t >= self.t1 for t, _ in self.rows):
+            time.sleep(0.01)
 
     def __exit__(self, *a):
         if self._p:
@@ -76,12 +92,17 @@ class ClockSampler:
             time.sleep(0.05)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        t0 = self.t0 if self.t0 is not None else float("-inf")
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        inside = [r for t, r in self.rows if t0 <= t <= t1 + 0.06]
+        if not inside and self.rows:  # region shorter than the sampling period: nearest row
+            inside = [min(self.rows, key=lambda tr: abs(tr[0] - 0.5 * (t0 + t1)))[1]]
+        sm = [float(r[0]) for r in inside if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in inside if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({names[i] for r in inside for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(inside)}
 
 
 def measured_peaks():
@@ -183,6 +204,7 @@ def run_ours(args, rank, world, local):
     launches0 = eng.stats()["kernel_launches"]
     k1_ms, k2_ms, step_ms = [], [], []
     with ClockSampler(local) as clocks:
+        clocks.mark_start()
         w0 = time.perf_counter()
         for s in range(args.steps):
             t1, t2 = step(args.warmup + s)
@@ -191,6 +213,7 @@ def run_ours(args, rank, world, local):
             step_ms.append(max(t1, t2))
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
+        clocks.mark_end()
     launches = eng.stats()["kernel_launches"] - launches0
     # parity spot check of the bench's own bytes (device copy == host source)
     ok = eng.checksum(N.KVF_TIER_DEVICE, dev_fixed[(args.warmup + args.steps - 1) % 2]) == \
