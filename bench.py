@@ -235,16 +235,23 @@ def run_ours(args, rank, world, local):
         q = torch.randn(2, 4 * heads, 128, device=f"cuda:{local}").to(torch.bfloat16)
         out = torch.empty_like(q)
         torch.cuda.synchronize()
-        per = []
+        per, chained = [], []
         for rep in range(4):
+            # one job per layer call ...
             js = [eng.attend(l, 4, q.data_ptr(), seqs, out.data_ptr(), 128 ** -0.5) for l in range(32)]
             eng.wait(js[-1])
             if rep:
                 per += [eng.elapsed_ms(j) for j in js]
             for j in js:
                 eng.release(j)
+            # ... and the decode step's 32 layers as one PDL-chained job (kvf_decode_attend_layers)
+            j = eng.attend_layers(0, 4, [q.data_ptr()] * 32, seqs, [out.data_ptr()] * 32, 128 ** -0.5)
+            eng.wait(j)
+            if rep:
+                chained.append(eng.elapsed_ms(j) / 32)
+            eng.release(j)
         k6_bytes = 2 * (FIXED + suffix) * 2 * eng.tpb
-        k6 = {"ms": statistics.median(per), "bytes": k6_bytes}
+        k6 = {"ms": statistics.median(chained), "ms_single": statistics.median(per), "bytes": k6_bytes}
     eng.close()
 
     # ---- e2e: the full workflow through the public API ---------------------------------
@@ -313,13 +320,15 @@ def run_ours(args, rank, world, local):
                          "peak": round(pcie["d2h"], 3), "unit": "GB/s",
                          "frac": round(wb_bytes / (mine["k2_avg_ms"] * 1e-3) / 1e9 / pcie["d2h"], 4),
                          "note": "rank 0; 16 MiB per launch, concurrent with the step's K1"},
-        # K6: decode attention reading the prefetched nodes in place, per layer call
-        # (job = descriptor-cache hit + main kernel + PDL combine, CUDA events on the compute stream)
+        # K6: decode attention reading the prefetched nodes in place, per layer of a
+        # decode step run as one chained job (kvf_decode_attend_layers: 32 x (main kernel + PDL
+        # combine), CUDA events on the compute stream); us_per_layer_call_single = one job per layer
         "roofline_k6": None if k6 is None else {
             "bound": "hbm", "kernel": "kvf_attend_kernel (K6 decode attention over slot runs)",
             "achieved": round(k6["bytes"] / (k6["ms"] * 1e-3) / 1e9, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(k6["bytes"] / (k6["ms"] * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
             "bytes_per_call": k6["bytes"], "us_per_layer_call": round(k6["ms"] * 1e3, 2),
+            "us_per_layer_call_single": round(k6["ms_single"] * 1e3, 2),
             "workload": "rank 0: 2 sequences x 8320 tokens (prefetched node + suffix), group 4, 32 layers"},
         "pcie_peaks_gbs": {k: round(v, 3) for k, v in pcie.items()},
         # the reference's own figure for this transfer is its cost model: 64e9 * 0.6 B/s + 50 us

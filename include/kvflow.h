@@ -14,6 +14,7 @@
  *   kvf_priority_propagate<- RadixCache::set_agent_priorities proj/src/radix_cache.cpp:266-285 [K4]
  *   kvf_victim_select     <- RadixCache::evict (selection) proj/src/radix_cache.cpp:302-372 [K5]
  *   kvf_decode_attend     <- (new) decode-side consumer of the slot-run table, SURVEY §8f-3 [K6]
+ *   kvf_decode_attend_layers <- the same for a decode step's layers as one chained job [K6]
  *   kvf_kv_append         <- (new) its write side: a layer's new K/V rows into slot runs
  *   kvf_peer_gather       <- (new) NVLink fetch from a replica's HBM, SURVEY §8f-4
  *   kvf_slots_alloc/free  <- (new) token-slot pools; the reference keeps only a byte ledger
@@ -250,6 +251,14 @@ int kvf_kv_append(kvf_engine* e, uint64_t job_id, uint32_t layer, const kvf_run*
 int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
                       const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale, void* out,
                       uint32_t chunk_tokens);
+/* A decode step's layers layer0 .. layer0+nlayers-1 as ONE job over the same run tables:
+ * q[l] / out[l] are layer (layer0 + l)'s buffers, laid out as for kvf_decode_attend.  The
+ * layers' kernels are chained with programmatic dependent launch, so layer l+1 starts on the
+ * SMs layer l has finished with; results are bit-identical to nlayers kvf_decode_attend
+ * calls.  The q / out pointer arrays are read during the call only. */
+int kvf_decode_attend_layers(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayers, uint32_t batch,
+                             uint32_t group, const void* const* q, const kvf_run* runs, const uint32_t* run_counts,
+                             float scale, void* const* out, uint32_t chunk_tokens);
 
 /* ---- payload (prefill emulation) and verification ----------------------------------- */
 /* Writes the deterministic payload of tokens with content ids cids[0..ntok) into the runs

@@ -112,6 +112,8 @@ _ENGINE_SIGS = {
                                     C.POINTER(C.c_uint64)]),
     "kvf_decode_attend": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                     C.POINTER(Run), C.c_void_p, C.c_float, C.c_void_p, C.c_uint32]),
+    "kvf_decode_attend_layers": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                           C.c_void_p, C.POINTER(Run), C.c_void_p, C.c_float, C.c_void_p, C.c_uint32]),
     "kvf_fill_payload": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_checksum": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.POINTER(C.c_uint64)]),
     "kvf_payload_checksum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),

@@ -25,7 +25,12 @@
 //    for the consumer too;
 //  * flash-decoding split: a sequence cut into k > 1 work items writes k unnormalised
 //    partials (m, l, o) and a combine kernel, launched with programmatic dependent launch
-//    so its launch overlaps the main kernel's tail, merges them; k = 1 writes out directly.
+//    so its launch overlaps the main kernel's tail, merges them; k = 1 writes out directly;
+//  * a decode step's layers chain (kvf_decode_attend_layers): every grid releases its
+//    dependents as soon as all its CTAs are resident and waits (griddepcontrol.wait) only
+//    before its first global write, so layer l+1's CTAs take the SMs layer l's fast CTAs
+//    free while its slow ones finish -- the per-SM bandwidth spread of one layer is hidden
+//    by the next instead of ending every layer.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -138,6 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned long long t_start = p.trace ? gtime() : 0;
+    // the dependent grid (this layer's combine, or the next layer) may be scheduled once every
+    // CTA of this one is resident; it waits before it writes anything (see the chain note)
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     // the item comes with the launch (parameter space) unless the grid is very large
     const AttnItem it = p.inline_items ? p.items_p[blockIdx.x] : p.items[blockIdx.x];
     // warp -> (head, sub-stream): the CTA's hpc heads x (8 / hpc) interleaved tile streams
@@ -275,6 +283,10 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
         __syncwarp();  // this ring slot is refilled next iteration
     }
     cp_async_wait<0>();
+    // everything above only read (q, the pool, the run tables); before the first write, the
+    // grid this one depends on (the previous layer's combine: it still reads the shared
+    // partials buffer) must be complete -- a no-op when launched without PDL
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (p.trace) {
         __syncthreads();
         if (tid == 0) {
@@ -316,9 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
                 p.part_ml[(pk + row) * 2 + 1] = l;
             }
         }
-        __syncthreads();
-        if (p.trace && tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
-        asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+        if (p.trace) {
+            __syncthreads();
+            if (tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
+        }
         return;
     }
     // ---- merge the warps of each head in shared memory (the rings are free once all are here)
@@ -377,23 +390,25 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
             }
         }
     }
-    // partials are written: the combine kernel (PDL secondary) may start consuming
-    __syncthreads();
-    if (p.trace && tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (p.trace) {
+        __syncthreads();
+        if (tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
+    }
 }
 
 // Merge a sequence's partials per (q head): out = sum_i e_i o_i / sum_i e_i l_i, e_i = 2^(m_i - M).
-// Launched as a programmatic dependent of the main kernel: griddepcontrol.wait releases it
-// once every CTA of the main kernel has published its partials.  One CTA per (sequence,
-// q head); its 8 warps split the partials (lane = 4 of the 128 dims), so a sequence cut into
-// ~150 items still merges in a few load round trips.
+// Launched as a programmatic dependent of the main kernel: its CTAs become resident next to
+// the main kernel's (<= 64 registers: 8 warps x 2 KiB + the main CTA's 48 K registers fill
+// one SM's 64 K) and griddepcontrol.wait releases them once the main kernel has completed.
+// One CTA per (sequence, q head); its 8 warps split the partials (lane = 4 of the 128 dims),
+// so a sequence cut into ~150 items still merges in a few load round trips.
 constexpr int kCombWarps = 8;
-__global__ void __launch_bounds__(kCombWarps * 32) kvf_attend_combine_kernel(const float* part_o, const float* part_ml,
+__global__ void __launch_bounds__(kCombWarps * 32, 4) kvf_attend_combine_kernel(const float* part_o, const float* part_ml,
                                                                             const uint32_t* seq_item0, uint32_t hkv,
                                                                             uint32_t group, __nv_bfloat16* out) {
     __shared__ float4 red_o[kCombWarps][32];
     __shared__ float red_x[kCombWarps], red_l[kCombWarps];
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // next layer: see the chain note
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const uint32_t b = blockIdx.x, hq = blockIdx.y;
     const uint32_t i0 = seq_item0[b], n = seq_item0[b + 1] - i0;
@@ -403,7 +418,7 @@ __global__ void __launch_bounds__(kCombWarps * 32) kvf_attend_combine_kernel(con
     // every warp pulls its first kRegs partials into registers at once (independent loads),
     // one block-wide max, then rescales from registers; partials beyond 8 x kRegs (a very long
     // sequence) take a second, load-then-scale pass
-    constexpr int kRegs = 8;
+    constexpr int kRegs = 6;
     float2 ml[kRegs];
     float4 ov[kRegs];
     float mloc = -INFINITY;
@@ -479,22 +494,25 @@ __global__ void kvf_attend_zero_kernel(const uint32_t* empty, uint32_t n, uint32
         out[empty[k / per] * per + k % per] = __float2bfloat16_rn(0.f);
 }
 
-}  // namespace
-
-extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
-                                 const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale,
-                                 void* out, uint32_t chunk_tokens) {
-    KVF_GUARD(e);
+// One job: layers layer0 .. layer0 + nlayers - 1 of a decode step over the same run tables
+// (q[l] / out[l] per layer).  Called with the engine lock held (KVF_GUARD).
+int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayers, uint32_t batch, uint32_t group,
+                const void* const* qs, const kvf_run* runs, const uint32_t* run_counts, float scale, void* const* outs,
+                uint32_t chunk_tokens) {
     if (e->geom.head_dim != kD || e->geom.dtype_bytes != 2)
         return set_error(KVF_E_INVALID_ARG, "kvf_decode_attend: head_dim 128, bf16 only");
-    if (layer >= e->geom.layers) return set_error(KVF_E_INVALID_ARG, "layer out of range");
+    if (nlayers == 0 || layer0 >= e->geom.layers || nlayers > e->geom.layers - layer0)
+        return set_error(KVF_E_INVALID_ARG, "layer out of range");
     if (group == 0 || group > kMaxGroup) return set_error(KVF_E_INVALID_ARG, "group must be 1..16");
     if (chunk_tokens && (chunk_tokens % kTok || chunk_tokens > kMaxChunk))
         return set_error(KVF_E_INVALID_ARG, "chunk_tokens must be a multiple of 16 in [16, 2048] (0 = auto)");
     if (batch == 0) return KVF_OK;
-    if (!q || !out || !run_counts) return set_error(KVF_E_INVALID_ARG, "null q / out / run_counts");
-    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(out)) & 3)
-        return set_error(KVF_E_INVALID_ARG, "q and out must be 4-byte aligned");
+    if (!qs || !outs || !run_counts) return set_error(KVF_E_INVALID_ARG, "null q / out / run_counts");
+    for (uint32_t l = 0; l < nlayers; ++l) {
+        if (!qs[l] || !outs[l]) return set_error(KVF_E_INVALID_ARG, "null q / out / run_counts");
+        if ((reinterpret_cast<uintptr_t>(qs[l]) | reinterpret_cast<uintptr_t>(outs[l])) & 3)
+            return set_error(KVF_E_INVALID_ARG, "q and out must be 4-byte aligned");
+    }
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
     const uint32_t hkv = e->geom.kv_heads_local, hq = hkv * group;
     const uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta));  // heads per CTA
@@ -655,14 +673,11 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
     prm.pool = e->dev_pool;
     prm.plane_stride = e->dev_slots * e->tpb;
     prm.tpb = static_cast<uint32_t>(e->tpb);
-    prm.layer = layer;
     prm.group = group;
     prm.hq = hq;
     prm.hkv = hkv;
     prm.hpc = hpc;
     prm.scale_log2 = scale * 1.4426950408889634f;
-    prm.q = static_cast<const __nv_bfloat16*>(q);
-    prm.out = static_cast<__nv_bfloat16*>(out);
     prm.items = reinterpret_cast<const AttnItem*>(ds);
     if (nitems <= kParamItems) {  // one wave: the items travel with the launch
         prm.inline_items = 1;
@@ -681,32 +696,47 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
     }
     static const char* trace_path = std::getenv("KVF_ATTEND_TRACE");
     unsigned long long* d_trace = nullptr;
-    if (trace_path && nitems) {
+    if (trace_path && nitems && nlayers == 1) {
         KVF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_trace), nitems * ygrid * 5 * 8, e->s_cmp));
         prm.trace = d_trace;
     }
-    if (nitems) {
-        kvf_attend_kernel<<<dim3(static_cast<uint32_t>(nitems), ygrid), kThreads, kSmemBytes, e->s_cmp>>>(prm);
-        KVF_CUDA(cudaGetLastError());
-        e->stats.kernel_launches++;
+    // the layer chain: attend(l) -> combine(l) -> attend(l + 1) -> ..., every launch after the
+    // first a programmatic dependent of the one before it (kernel-side protocol: see the top)
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    for (uint32_t l = 0; l < nlayers; ++l) {
+        prm.layer = layer0 + l;
+        prm.q = static_cast<const __nv_bfloat16*>(qs[l]);
+        prm.out = static_cast<__nv_bfloat16*>(outs[l]);
+        if (nitems) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<uint32_t>(nitems), ygrid);
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = kSmemBytes;
+            cfg.stream = e->s_cmp;
+            cfg.attrs = pdl;
+            cfg.numAttrs = l ? 1 : 0;
+            KVF_CUDA(cudaLaunchKernelEx(&cfg, kvf_attend_kernel, prm));
+            e->stats.kernel_launches++;
+        }
+        if (multi) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(batch, hq);
+            cfg.blockDim = dim3(kCombWarps * 32);
+            cfg.stream = e->s_cmp;
+            cfg.attrs = pdl;
+            cfg.numAttrs = 1;
+            KVF_CUDA(cudaLaunchKernelEx(&cfg, kvf_attend_combine_kernel, static_cast<const float*>(prm.part_o),
+                                        static_cast<const float*>(prm.part_ml), d_seq_item0, hkv, group, prm.out));
+            e->stats.kernel_launches++;
+        }
     }
-    if (multi) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(batch, hq);
-        cfg.blockDim = dim3(kCombWarps * 32);
-        cfg.stream = e->s_cmp;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        KVF_CUDA(cudaLaunchKernelEx(&cfg, kvf_attend_combine_kernel, static_cast<const float*>(prm.part_o),
-                                    static_cast<const float*>(prm.part_ml), d_seq_item0, hkv, group, prm.out));
-        e->stats.kernel_launches++;
-    }
-    if (nempty) {
+    // empty sequences (rows no other kernel writes): after the chain
+    for (uint32_t l = 0; nempty && l < nlayers; ++l) {
         kvf_attend_zero_kernel<<<static_cast<uint32_t>(std::min<uint64_t>(1024, (nempty * hq * kD + 255) / 256)), 256, 0,
-                                 e->s_cmp>>>(d_empty, static_cast<uint32_t>(nempty), hq, prm.out);
+                                 e->s_cmp>>>(d_empty, static_cast<uint32_t>(nempty), hq,
+                                             static_cast<__nv_bfloat16*>(outs[l]));
         KVF_CUDA(cudaGetLastError());
         e->stats.kernel_launches++;
     }
@@ -724,8 +754,25 @@ extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer,
             std::fclose(f);
         }
     }
-    j.bytes = total_tok * 2 * e->tpb;  // K + V of one layer, read once
+    j.bytes = total_tok * 2 * e->tpb * nlayers;  // K + V of each layer, read once
     e->stats.attend_bytes += j.bytes;
-    e->stats.attend_calls++;
+    e->stats.attend_calls += nlayers;
     return end_job(e, job_id, j);
+}
+
+}  // namespace
+
+extern "C" int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
+                                 const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale,
+                                 void* out, uint32_t chunk_tokens) {
+    KVF_GUARD(e);
+    return attend_impl(e, job_id, layer, 1, batch, group, &q, runs, run_counts, scale, &out, chunk_tokens);
+}
+
+extern "C" int kvf_decode_attend_layers(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayers,
+                                        uint32_t batch, uint32_t group, const void* const* q, const kvf_run* runs,
+                                        const uint32_t* run_counts, float scale, void* const* out,
+                                        uint32_t chunk_tokens) {
+    KVF_GUARD(e);
+    return attend_impl(e, job_id, layer0, nlayers, batch, group, q, runs, run_counts, scale, out, chunk_tokens);
 }

@@ -194,6 +194,20 @@ class Engine:
                                             float(scale), out_ptr, chunk))
         return job
 
+    def attend_layers(self, layer0, group, q_ptrs, seq_runs, out_ptrs, scale, job=None, chunk=0):
+        """K6 for a decode step's layers layer0 .. layer0+len(q_ptrs)-1 as one chained job
+        (q_ptrs[l] / out_ptrs[l]: that layer's device buffers, as for attend())."""
+        if len(q_ptrs) != len(out_ptrs):
+            raise ValueError("one q and one out pointer per layer")
+        job = job or self.new_job()
+        flat, counts = seq_runs if isinstance(seq_runs, tuple) else self.attend_runs(seq_runs)
+        qa = (C.c_void_p * max(1, len(q_ptrs)))(*q_ptrs)
+        oa = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
+        N.check(self._lib.kvf_decode_attend_layers(self.h, job, layer0, len(q_ptrs), len(counts), group, qa,
+                                                   C.cast(flat.ctypes.data, C.POINTER(N.Run)), counts.ctypes.data,
+                                                   float(scale), oa, chunk))
+        return job
+
     def query(self, job):
         d = C.c_int32()
         N.check(self._lib.kvf_job_query(self.h, job, C.byref(d)))

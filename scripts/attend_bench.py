@@ -61,6 +61,15 @@ def step(e, seqs, q, out, group, layers, scale):
     return ms, per
 
 
+def step_chained(e, seqs, q, out, group, layers, scale):
+    """The decode step's layers as one kvf_decode_attend_layers job (PDL-chained)."""
+    j = e.attend_layers(0, group, [q.data_ptr()] * layers, e.attend_runs(seqs), [out.data_ptr()] * layers, scale)
+    e.wait(j)
+    ms = e.elapsed_ms(j)
+    e.release(j)
+    return ms
+
+
 def run(name, kv_local, group, lens, piece=None, steps=5, layers=32):
     rng = np.random.default_rng(1)
     total = sum(lens)
@@ -80,6 +89,7 @@ def run(name, kv_local, group, lens, piece=None, steps=5, layers=32):
         ms, per = step(e, seqs, q, out, group, layers, scale)
         spans.append(ms)
         pers += per
+    chained = [step_chained(e, seqs, q, out, group, layers, scale) for _ in range(steps + 2)][2:]
     bytes_layer = total * 2 * e.tpb
     # compaction comparator: K3 gathers every sequence (all layers) into staging, then attend
     st = torch.empty(max(lens) * e.token_bytes, dtype=torch.uint8, device="cuda")
@@ -104,6 +114,10 @@ def run(name, kv_local, group, lens, piece=None, steps=5, layers=32):
             "step_ms": round(step_ms, 4), "layer_call_ms_median": round(layer_ms, 4),
             "achieved_GBps": round(gbs, 1), "step_GBps": round(bytes_layer * layers / (step_ms * 1e-3) / 1e9, 1),
             "hbm_peak_GBps": peak, "peak_source": src, "frac": round(gbs / peak, 4),
+            "chained_step_ms": round(min(chained), 4),
+            "chained_layer_us": round(min(chained) / layers * 1e3, 2),
+            "chained_GBps": round(bytes_layer * layers / (min(chained) * 1e-3) / 1e9, 1),
+            "chained_frac": round(bytes_layer * layers / (min(chained) * 1e-3) / 1e9 / peak, 4),
             "compaction_k3_ms_per_step": round(min(k3), 3),
             "in_place_saves": f"{min(k3):.2f} ms of K3 copies per step ({2 * bytes_layer * layers / 1e9:.2f} GB moved)"}
 

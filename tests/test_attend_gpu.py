@@ -192,6 +192,68 @@ def test_attend_errors():
             e.attend(0, 4, q.data_ptr(), [[(0, 10)]], out.data_ptr(), 1.0)    # head_dim 128 only
 
 
+@pytest.mark.parametrize("kv_local,group,chunk,lens", [
+    (8, 4, 0, [8320, 8320]),                      # the bench's C2 shape: partials + combine
+    (8, 4, 0, [1, 15, 0, 100, 1000, 4097, 300]),  # ragged, an empty sequence
+    (8, 4, 0, [10, 20, 33]),                      # one item per sequence: no combine, attend -> attend
+    (2, 8, 64, [700, 5, 1500]),                   # 4 CTA rows (hpc 2), explicit chunk
+    (1, 8, 0, [3000, 12]),                        # 70B shard
+])
+def test_attend_layers_chain(kv_local, group, chunk, lens):
+    """kvf_decode_attend_layers: a decode step's layers as one PDL-chained job.  Bit-identical
+    to one kvf_decode_attend call per layer (same kernels, same items; the chain only changes
+    when each grid starts), and within tolerance of the fp32 reference; repeated back to back
+    (a chain race would show as a changed bit)."""
+    need_gpu()
+    rng = np.random.default_rng(sum(lens) + kv_local)
+    torch.manual_seed(kv_local * 13 + group)
+    layers = 6
+    with Engine(layers=layers, kv_heads_total=8, kv_heads_local=kv_local, head_offset=0,
+                gpu_slots=sum(lens) * 2 + 4096, host_slots=0) as e:
+        seq_runs, kvs = [], []
+        for i, n in enumerate(lens):
+            if n == 0:
+                seq_runs.append([])
+                kvs.append(None)
+                continue
+            runs = fragmented_runs(e, n, rng, max_piece=[5000, 60, 700][i % 3])
+            kv = torch.randn(2 * layers, n, kv_local, 128, device="cuda").to(torch.bfloat16)
+            write_runs(e, runs, kv)
+            seq_runs.append(runs)
+            kvs.append(kv)
+        B, hq = len(lens), kv_local * group
+        packed = e.attend_runs(seq_runs)
+        scale = 1.0 / math.sqrt(128)
+        q = torch.randn(layers, B, hq, 128, device="cuda").to(torch.bfloat16)
+        single = torch.full((layers, B, hq, 128), float("nan"), device="cuda", dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        for l in range(layers):
+            j = e.attend(l, group, q[l].data_ptr(), packed, single[l].data_ptr(), scale, chunk=chunk)
+            e.wait(j)
+            e.release(j)
+        for l in range(layers):
+            check(single[l], reference(q[l], kvs, l, group, scale))
+        qp = [q[l].data_ptr() for l in range(layers)]
+        for rep in range(8):
+            chained = torch.full_like(single, float("nan"))
+            torch.cuda.synchronize()
+            j = e.attend_layers(0, group, qp, packed, [chained[l].data_ptr() for l in range(layers)], scale,
+                                chunk=chunk)
+            e.wait(j)
+            e.release(j)
+            assert torch.equal(chained.view(torch.int16), single.view(torch.int16)), f"rep {rep}"
+        # a sub-range of layers, every layer writing the SAME out buffer: the last layer's wins
+        same = torch.full_like(single[0], float("nan"))
+        j = e.attend_layers(2, group, qp[2:5], packed, [same.data_ptr()] * 3, scale, chunk=chunk)
+        e.wait(j)
+        e.release(j)
+        assert torch.equal(same.view(torch.int16), single[4].view(torch.int16))
+        with pytest.raises(N.KvfError):
+            e.attend_layers(4, group, qp[:3], packed, [same.data_ptr()] * 3, scale)  # layers 4..6 of 6
+        with pytest.raises(N.KvfError):
+            e.attend_layers(0, group, [qp[0], 0], packed, [same.data_ptr()] * 2, scale)  # null q
+
+
 @pytest.mark.parametrize("kv_local", [8, 2])
 def test_append_then_decode_attend(kv_local):
     """kvf_kv_append writes a layer's K/V rows ([ntok][heads][128], the model's layout) into
