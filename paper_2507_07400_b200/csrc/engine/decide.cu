@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine_internal.hpp"
@@ -530,8 +532,26 @@ int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
 // outputs (publish_done); the host spins on it instead of cudaStreamSynchronize -- the
 // result is usable one posted PCIe write after the kernel's last store.  A fault surfaces
 // through the periodic cudaStreamQuery.  Kernel time comes from its own globaltimer stamps.
+// KVF_DECISION_TRACE=<file>: one line per fast-path call -- host phases (entry -> launch
+// call -> launch returned -> done word seen) and the kernel's globaltimer start / end
+// against the host's CLOCK_REALTIME at the launch call (globaltimer counts Unix-epoch ns on
+// this driver; the idle rows check that).  Diagnostics only.
+struct DecisionTrace {
+    std::chrono::steady_clock::time_point t_launch, t_launched;
+    long long rt_launch_ns = 0;
+};
+const char* decision_trace_path() {
+    static const char* p = std::getenv("KVF_DECISION_TRACE");
+    return p;
+}
+long long realtime_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::system_clock::now().time_since_epoch())
+        .count();
+}
+
 int spin_decision(kvf_engine* e, const unsigned long long* hdr, unsigned long long seq,
-                  std::chrono::steady_clock::time_point t0) {
+                  std::chrono::steady_clock::time_point t0, const DecisionTrace* tr = nullptr, const char* kind = "",
+                  uint32_t n = 0) {
     const volatile unsigned long long* flag = hdr + kDoneWord;
     // a faulted kernel never publishes: look at the stream only after 200 us, then every 100 us
     // (a driver call inside the normal ~10-30 us wait would only delay seeing the done word)
@@ -550,8 +570,21 @@ int spin_decision(kvf_engine* e, const unsigned long long* hdr, unsigned long lo
 #endif
     }
     e->stats.decision_kernel_ms += static_cast<double>(hdr[8] - hdr[3]) * 1e-6;
-    e->stats.decision_call_us +=
-        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    const auto t_done = std::chrono::steady_clock::now();
+    e->stats.decision_call_us += std::chrono::duration<double, std::micro>(t_done - t0).count();
+    if (tr && decision_trace_path()) {
+        const long long rt_done = realtime_ns();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        if (FILE* f = std::fopen(decision_trace_path(), "a")) {
+            std::fprintf(f,
+                         "{\"kind\": \"%s\", \"n\": %u, \"pack_us\": %.2f, \"launch_call_us\": %.2f, \"spin_us\": %.2f, "
+                         "\"kstart_after_launch_us\": %.2f, \"kernel_us\": %.2f, \"seen_after_kend_us\": %.2f}\n",
+                         kind, n, us(t0, tr->t_launch), us(tr->t_launch, tr->t_launched), us(tr->t_launched, t_done),
+                         (static_cast<long long>(hdr[3]) - tr->rt_launch_ns) * 1e-3, (hdr[8] - hdr[3]) * 1e-3,
+                         (rt_done - static_cast<long long>(hdr[8])) * 1e-3);
+            std::fclose(f);
+        }
+    }
     return KVF_OK;
 }
 
@@ -612,14 +645,20 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
                                       static_cast<int>(kPrioSmemNodes * 8 + kZeroCopyBytes + 64)));
         e->prio_attr_set = true;
     }
+    DecisionTrace tr;
+    if (decision_trace_path()) {
+        tr.t_launch = std::chrono::steady_clock::now();
+        tr.rt_launch_ns = realtime_ns();
+    }
     kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
                                                          zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
                                                          zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq);
     KVF_CUDA(cudaGetLastError());
+    if (decision_trace_path()) tr.t_launched = std::chrono::steady_clock::now();
     e->stats.kernel_launches++;
     e->stats.decisions++;
     if (zero_copy) {
-        if (int src = spin_decision(e, h_hdr, seq, t0)) return src;
+        if (int src = spin_decision(e, h_hdr, seq, t0, &tr, "k4", n)) return src;
         std::memcpy(out_rank, h + out_off, n * 8);
         return KVF_OK;
     }
@@ -703,16 +742,23 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
         __atomic_store_n(reinterpret_cast<unsigned long long*>(h + ((used + 255) & ~size_t(255))) + kDoneWord, 0ull,
                          __ATOMIC_RELEASE);
     if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
+    DecisionTrace tr;
+    if (decision_trace_path()) {
+        tr.t_launch = std::chrono::steady_clock::now();
+        tr.rt_launch_ns = realtime_ns();
+    }
     kvf_victim_kernel<<<1, victim_threads(n), smem, e->s_dec>>>(td, rq, od, seq);
     if (const cudaError_t le = cudaGetLastError(); le != cudaSuccess)
         return cuda_error(le, ("K5 launch (n=" + std::to_string(n) + " threads=" + std::to_string(victim_threads(n)) +
                                " smem=" + std::to_string(smem) + " zero_copy=" + std::to_string(zero_copy) + ")")
                                   .c_str());
+    if (decision_trace_path()) tr.t_launched = std::chrono::steady_clock::now();
     e->stats.kernel_launches++;
     e->stats.decisions++;
     char* hout = h + ((used + 255) & ~size_t(255));
     if (zero_copy) {
-        if (int src = spin_decision(e, reinterpret_cast<const unsigned long long*>(hout), seq, t0)) return src;
+        if (int src = spin_decision(e, reinterpret_cast<const unsigned long long*>(hout), seq, t0, &tr, "k5", n))
+            return src;
     } else {
         KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
         KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));

@@ -681,6 +681,17 @@ uint32_t grid_for(const kvf_engine* e, uint64_t work, uint32_t threads) {
     return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(g, static_cast<uint64_t>(e->sm_count) * 8)));
 }
 
+// Short-lived CTAs (~per_thread items each) for bulk work that runs while decisions must
+// start promptly: a grid-stride grid of sm_count x 8 resident CTAs holds every SM's thread
+// slots for the whole kernel (a 1 GiB prompt fill: ~0.65 ms), so a K4/K5 CTA on the
+// high-priority decision stream waited for the fill to END (measured: 665 us late starts,
+// scripts/decision_trace.py).  With CTAs of a few us the block scheduler hands the next free
+// slot to the decision CTA.
+uint32_t grid_short(uint64_t work, uint32_t threads, uint32_t per_thread) {
+    const uint64_t g = (work + static_cast<uint64_t>(threads) * per_thread - 1) / (static_cast<uint64_t>(threads) * per_thread);
+    return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(g, 0x7fffffffull)));
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -1212,7 +1223,7 @@ int kvf_fill_payload(kvf_engine* e, int32_t tier, const kvf_run* runs, uint32_t 
     int rc = stage_slots(e, runs, n, cids, ntok, &d_slots, &d_cids);
     if (rc) return rc;
     const uint64_t words = static_cast<uint64_t>(e->planes) * ntok * (e->tpb / 8);
-    kvf_fill_kernel<<<grid_for(e, words, 256), 256, 0, e->s_dev>>>(
+    kvf_fill_kernel<<<grid_short(words, 256, 16), 256, 0, e->s_dev>>>(
         tier_base(e, tier), tier_slots(e, tier) * e->tpb, static_cast<uint32_t>(e->tpb), e->planes,
         e->geom.head_dim / 4, e->geom.head_offset, d_slots, d_cids, ntok);
     KVF_CUDA(cudaGetLastError());
