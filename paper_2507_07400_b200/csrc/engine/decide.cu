@@ -16,7 +16,8 @@
 //     One CTA, everything in shared memory: a bitonic sort of the candidates by the
 //     4-word key, R and eff by parallel root walks (shared-memory atomics with early
 //     exit, no per-level barriers), a bitonic sort of 64-bit (eff, depth, idx) keys, and
-//     a block scan for the byte cut.
+//     a block scan for the byte cut.  Both sorts hold one to four elements per thread in
+//     registers (bitonic_reg): only the stages spanning more than a warp touch shared memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "engine_internal.hpp"
 
@@ -171,27 +173,107 @@ __host__ __device__ inline uint32_t pow2_ceil(uint32_t x) {
 #endif
 }
 
-// Bitonic sort over P (power of two) elements with one compare-exchange per pair index.
-// Pair p -> (i, i|j) with i = insert-zero-bit(p, log2 j).  Each warp owns a 32-aligned range
-// of pair indices, so stages with j <= 32 touch only that warp's 64-element chunk and need
-// just __syncwarp; only j >= 64 stages pay a block barrier (15 of 66 stages at P = 2048).
-template <typename Greater, typename Swap>
-__device__ __forceinline__ void bitonic(uint32_t P, Greater greater, Swap swap) {
-    __syncthreads();
-    for (uint32_t k = 2; k <= P; k <<= 1)
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 64) __syncthreads();
-            for (uint32_t pr = threadIdx.x; pr < P / 2; pr += blockDim.x) {
-                const uint32_t i = ((pr & ~(j - 1)) << 1) | (pr & (j - 1));
-                const uint32_t l = i | j;
-                const bool up = (i & k) == 0;
-                if (up ? greater(i, l) : greater(l, i)) swap(i, l);
+// Bitonic sort with the elements in registers: thread t holds positions t*E .. t*E+E-1
+// (x[]), P / E threads take part (a multiple of 32: P >= 128, E <= 4).  Per merge level k,
+// stages with j >= 32E run as compare-exchanges in shared memory (ld/st: position ->
+// element), stages E <= j < 32E exchange with lane t ^ (j/E) through shuffles, and j < E
+// inside the thread -- at P = 512 35 of 45 stages never touch shared memory or a barrier
+// (an all-shared-memory network spent ~870 cycles per stage there).
+// after(a, b): a must come after b (a total order, or identical elements).
+template <int E, typename V, typename After, typename Ld, typename St, typename Shfl>
+__device__ __forceinline__ void bitonic_reg(uint32_t P, V (&x)[E], After after, Ld ld, St st, Shfl shfl) {
+    const uint32_t t = threadIdx.x;
+    const bool act = t * E < P;  // warp-uniform
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        uint32_t j = k >> 1;
+        if (j >= 32u * E) {
+            if (act) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) st(t * E + e, x[e]);
             }
-            if (j >= 64) __syncthreads();
-            else __syncwarp();
+            __syncthreads();
+            for (; j >= 32u * E; j >>= 1) {
+                for (uint32_t pr = t; pr < P / 2; pr += blockDim.x) {
+                    const uint32_t i = ((pr & ~(j - 1)) << 1) | (pr & (j - 1));
+                    const uint32_t l = i | j;
+                    const V a = ld(i), b = ld(l);
+                    if ((i & k) == 0 ? after(a, b) : after(b, a)) {
+                        st(i, b);
+                        st(l, a);
+                    }
+                }
+                __syncthreads();
+            }
+            // own positions only: the next round's stores (own positions again) and its
+            // shared stages (after a barrier) cannot race these loads
+            if (act) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) x[e] = ld(t * E + e);
+            }
         }
-    __syncthreads();
+        if (act) {
+            for (; j >= static_cast<uint32_t>(E); j >>= 1) {  // across lanes
+                const uint32_t m = j / E;
+                const bool lower = (t & m) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const V y = shfl(x[e], m);
+                    const bool up = ((t * E + e) & k) == 0;
+                    const bool x_after_y = after(x[e], y);
+                    // the lower position of an ascending pair keeps the smaller element
+                    if ((lower == up) == x_after_y) x[e] = y;
+                }
+            }
+            // inside the thread: j = min(k/2, E/2) .. 1, unrolled so x[] stays in registers
+#pragma unroll
+            for (int jj = E / 2; jj > 0; jj >>= 1) {
+                if (static_cast<uint32_t>(jj) > (k >> 1)) continue;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (e & jj) continue;
+                    const int l = e | jj;
+                    const bool up = ((t * E + e) & k) == 0;
+                    if (up ? after(x[e], x[l]) : after(x[l], x[e])) {
+                        const V tmp = x[e];
+                        x[e] = x[l];
+                        x[l] = tmp;
+                    }
+                }
+            }
+        }
+    }
 }
+
+// Sort positions [0, P) of (ld, st) with bitonic_reg; out(position, element) receives the
+// sorted sequence (from registers).  The caller fills [c, P) with pads that sort last.
+template <typename V, typename After, typename Ld, typename St, typename Shfl, typename Out>
+__device__ __forceinline__ void sort_reg(uint32_t P, After after, Ld ld, St st, Shfl shfl, Out out) {
+    auto run = [&](auto tag) {
+        constexpr int E = decltype(tag)::value;
+        const uint32_t t = threadIdx.x;
+        V x[E];
+        __syncthreads();  // the pads / inputs are in place
+        if (t * E < P) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) x[e] = ld(t * E + e);
+        }
+        bitonic_reg<E>(P, x, after, ld, st, shfl);
+        __syncthreads();  // every shared stage has been read before out() may reuse the arrays
+        if (t * E < P) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) out(t * E + e, x[e]);
+        }
+        __syncthreads();
+    };
+    if (P <= blockDim.x) run(std::integral_constant<int, 1>{});
+    else if (P == 2 * blockDim.x) run(std::integral_constant<int, 2>{});
+    else run(std::integral_constant<int, 4>{});
+}
+
+struct Cand {  // phase-2 element: primary key words and the node index (0xFFFF = pad)
+    uint64_t a, b;
+    uint32_t s;
+};
 
 // Rank sort for <= 64 elements: element i's output position is the number of elements that
 // sort before it.  G = blockDim.x / 64 consecutive lanes share element i and split the j range,
@@ -353,28 +435,29 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
         if (i != 0xFFFFFFFFu) ord[sel[i]] = static_cast<int32_t>(rk);
         __syncthreads();
     } else {
-        bitonic(
-        P,
-        [&](uint32_t a, uint32_t b) {  // element at a must come after element at b
-            const uint32_t x = sel[a], y = sel[b];
-            if (x == 0xFFFFu || y == 0xFFFFu) return x == 0xFFFFu && y != 0xFFFFu;
-            if (!slow) {
-                if (pk0[a] != pk0[b]) return pk0[a] > pk0[b];
-                if (pk1[a] != pk1[b]) return pk1[a] > pk1[b];
-            }
-            return full_after(x, y);
-        },
-        [&](uint32_t a, uint32_t b) {
-            const uint16_t s0 = sel[a];
-            sel[a] = sel[b];
-            sel[b] = s0;
-            const uint64_t p0 = pk0[a], p1 = pk1[a];
-            pk0[a] = pk0[b];
-            pk1[a] = pk1[b];
-            pk0[b] = p0;
-            pk1[b] = p1;
-        });
-        for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) ord[sel[k]] = static_cast<int32_t>(k);
+        sort_reg<Cand>(
+            P,
+            [&](const Cand& x, const Cand& y) {  // x must come after y
+                if (x.s == 0xFFFFu || y.s == 0xFFFFu) return x.s == 0xFFFFu && y.s != 0xFFFFu;
+                if (!slow) {
+                    if (x.a != y.a) return x.a > y.a;
+                    if (x.b != y.b) return x.b > y.b;
+                }
+                return full_after(x.s, y.s);
+            },
+            [&](uint32_t i) { return Cand{pk0[i], pk1[i], sel[i]}; },
+            [&](uint32_t i, const Cand& v) {
+                pk0[i] = v.a;
+                pk1[i] = v.b;
+                sel[i] = static_cast<uint16_t>(v.s);
+            },
+            [](const Cand& v, uint32_t m) {
+                return Cand{__shfl_xor_sync(0xffffffffu, v.a, m), __shfl_xor_sync(0xffffffffu, v.b, m),
+                            __shfl_xor_sync(0xffffffffu, v.s, m)};
+            },
+            [&](uint32_t pos, const Cand& v) {
+                if (v.s != 0xFFFFu) ord[v.s] = static_cast<int32_t>(pos);
+            });
     }
     stamp(2);
     // 3. blocked(n): some node of n's device subtree (below n) is not self-eligible or would
@@ -433,13 +516,11 @@ __global__ void __launch_bounds__(kThreads) kvf_victim_kernel(const TreeDev t_in
         keys = pref;
         pref = tmp;
     } else {
-        bitonic(
-            PR, [&](uint32_t a, uint32_t b) { return keys[a] > keys[b]; },
-            [&](uint32_t a, uint32_t b) {
-                const uint64_t x = keys[a];
-                keys[a] = keys[b];
-                keys[b] = x;
-            });
+        sort_reg<uint64_t>(
+            PR, [](uint64_t x, uint64_t y) { return x > y; }, [&](uint32_t i) { return keys[i]; },
+            [&](uint32_t i, uint64_t v) { keys[i] = v; },
+            [](uint64_t v, uint32_t m) { return __shfl_xor_sync(0xffffffffu, v, m); },
+            [&](uint32_t pos, uint64_t v) { keys[pos] = v; });
     }
     stamp(4);
     // 6. exclusive byte prefix in victim order (block scan)
@@ -514,9 +595,9 @@ size_t victim_smem(uint32_t n, size_t blob = 0) {
            3 * ((n + 15) & ~15u) + 64 + (blob ? blob + 32 : 0);
 }
 
-uint32_t victim_threads(uint32_t n) {  // one compare-exchange per thread per sort stage
-    const uint32_t half = pow2_ceil(n > 1 ? n : 2) / 2;
-    return half < 128 ? 128 : (half > static_cast<uint32_t>(kThreads) ? kThreads : half);
+uint32_t victim_threads(uint32_t n) {  // one sort element per thread up to 1024 (sort_reg: E <= 4)
+    const uint32_t pn = pow2_ceil(n > 1 ? n : 2);
+    return pn < 128 ? 128 : (pn > static_cast<uint32_t>(kThreads) ? kThreads : pn);
 }
 
 int finish_decision(kvf_engine* e, std::chrono::steady_clock::time_point t0) {
