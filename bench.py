@@ -404,9 +404,22 @@ def cpu_baseline(node_bytes, heads):
                          runs_array([(0, ntok)]), 1, threads)
         done += 1
     el = time.perf_counter() - t0
+    # the same restatement at T = 1, 2, 4, ... nproc threads (~0.5 s each)
+    sweep, T = {}, 1
+    while True:
+        n, s0 = 0, time.perf_counter()
+        while n == 0 or time.perf_counter() - s0 < 0.5:
+            L.kvfo_copy_runs(C.byref(g), src.ctypes.data, ntok, runs_array([(0, ntok)]), 1, dst.ctypes.data, ntok,
+                             runs_array([(0, ntok)]), 1, T)
+            n += 1
+        sweep[str(T)] = round(n * node_bytes / (time.perf_counter() - s0) / 1e9, 2)
+        if T >= threads:
+            break
+        T = min(threads, T * 2)
     dec_s, _, dec_kind = reference_decisions(reps=5)
     return {"value": round(done * node_bytes / el / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "port",
             "sample": f"{done} x 8192-token (1 GiB) node copies host->host via kvfo_copy_runs, {el:.1f} s",
+            "threads_sweep_gbs": sweep,
             # the latency half of the metric: the UNMODIFIED reference Simulator's whole C2 run
             # (44 agent steps: priorities, evictions, prefetch issue, event loop) on one host core
             "reference_decisions_us_per_agent_step": None if dec_s is None else round(dec_s / 44 * 1e6, 2),
