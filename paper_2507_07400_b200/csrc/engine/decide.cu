@@ -731,7 +731,9 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
         tr.t_launch = std::chrono::steady_clock::now();
         tr.rt_launch_ns = realtime_ns();
     }
-    kvf_priority_kernel<<<1, kThreads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
+    // sized to the tree (128..1024 threads): a small CTA also fits beside a K6 CTA on a busy SM
+    const uint32_t prio_threads = std::min<uint32_t>(kThreads, std::max<uint32_t>(128, pow2_ceil(std::max(n, m))));
+    kvf_priority_kernel<<<1, prio_threads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
                                                          zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
                                                          zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq);
     KVF_CUDA(cudaGetLastError());
