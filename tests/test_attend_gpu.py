@@ -198,6 +198,7 @@ def test_attend_errors():
     (8, 4, 0, [10, 20, 33]),                      # one item per sequence: no combine, attend -> attend
     (2, 8, 64, [700, 5, 1500]),                   # 4 CTA rows (hpc 2), explicit chunk
     (1, 8, 0, [3000, 12]),                        # 70B shard
+    (8, 4, 0, [0, 0, 0]),                         # every sequence empty: zero rows only, no attend grid
 ])
 def test_attend_layers_chain(kv_local, group, chunk, lens):
     """kvf_decode_attend_layers: a decode step's layers as one PDL-chained job.  Bit-identical
@@ -242,6 +243,12 @@ def test_attend_layers_chain(kv_local, group, chunk, lens):
             e.wait(j)
             e.release(j)
             assert torch.equal(chained.view(torch.int16), single.view(torch.int16)), f"rep {rep}"
+        # one layer through the chained entry point == the single-layer call
+        one = torch.full_like(single[0], float("nan"))
+        j = e.attend_layers(3, group, qp[3:4], packed, [one.data_ptr()], scale, chunk=chunk)
+        e.wait(j)
+        e.release(j)
+        assert torch.equal(one.view(torch.int16), single[3].view(torch.int16))
         # a sub-range of layers, every layer writing the SAME out buffer: the last layer's wins
         same = torch.full_like(single[0], float("nan"))
         j = e.attend_layers(2, group, qp[2:5], packed, [same.data_ptr()] * 3, scale, chunk=chunk)
