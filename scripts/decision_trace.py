@@ -17,6 +17,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 TRACE = os.path.join(tempfile.mkdtemp(), "dtrace.jsonl")
 os.environ["KVF_DECISION_TRACE"] = TRACE  # read once, at the first decision call
+ARRIVALS = os.path.join(os.path.dirname(TRACE), "arrivals.jsonl")
+os.environ["KVF_ARRIVAL_TRACE"] = ARRIVALS  # per-arrival phases (Simulator::on_arrival)
 
 from oracle_ffi import load_jsonl  # noqa: E402
 from paper_2507_07400_b200 import _native as N  # noqa: E402
@@ -90,6 +92,12 @@ def main():
         {**{k: round(r[k], 2) for k in KEYS if k != "kstart_after_launch_us"}, "kind": r["kind"], "n": r["n"], "index": i,
          "kstart_delay_vs_median_us": round(r["kstart_after_launch_us"] - typ, 2)}
         for i, r in enumerate(wf) if r["pack_us"] + r["launch_call_us"] + r["spin_us"] > 60]
+    arr = [json.loads(x) for x in open(ARRIVALS)] if os.path.exists(ARRIVALS) else []
+    if arr:
+        res["c2_arrivals"] = {"count": len(arr), "us_median": round(statistics.median(a["us"] for a in arr), 2),
+                              "us_mean": round(statistics.mean(a["us"] for a in arr), 2),
+                              "slowest": sorted(arr, key=lambda a: -a["us"])[:4],
+                              "first": arr[:2]}
     res["note"] = ("per call, medians: pack = entry -> launch call; launch_call = cudaLaunchKernel; spin = launch "
                    "returned -> done word seen; kstart_after_launch = kernel globaltimer start - host realtime at "
                    "the launch call; kernel = in-kernel (globaltimer); seen_after_kend = host realtime when the "
