@@ -15,6 +15,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "engine_internal.hpp"
@@ -249,10 +250,23 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
     int32_t* o_idx = reinterpret_cast<int32_t*>(hout_dev + 256);
     uint8_t* o_act = reinterpret_cast<uint8_t*>(hout_dev + 256 + ((np * 4ull + 255) & ~255ull));
 
-    const uint64_t key = (static_cast<uint64_t>(np) << 1) | (wa ? 1u : 0u);
+    // node ids and access sequence numbers are counters: their LSD passes only need the bytes
+    // the largest one uses (8 CUB passes per 64-bit word otherwise; padding nodes hold 0)
+    uint64_t max_id = 0, max_seq = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        max_id = std::max(max_id, t->id[i]);
+        max_seq = std::max(max_seq, t->seq[i]);
+    }
+    auto live_bytes = [](uint64_t x) {
+        uint32_t b = 1;
+        while (b < 8 && (x >> (8 * b))) ++b;
+        return b;
+    };
+    const uint32_t id_bytes = live_bytes(max_id), seq_bytes = live_bytes(max_seq);
+    const uint64_t key = (static_cast<uint64_t>(np) << 9) | (id_bytes << 5) | (seq_bytes << 1) | (wa ? 1u : 0u);
     auto git = e->big_graphs.find(key);
     if (git == e->big_graphs.end()) {
-        // ---- capture the whole device-wide sequence once per (bucket, policy) ----
+        // ---- capture the whole device-wide sequence once per (bucket, policy, id / seq widths) ----
         char* d = static_cast<char*>(e->ws_big.dev);
         char* dp = d;
         const BigReq* dreq = take<BigReq>(dp, 1);
@@ -290,8 +304,9 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
         big_stage<<<grid, threads, 0, s>>>(bt, dreq, flags, blocked, vals_a);
         for (int w = 0; w < (wa ? 4 : 3); ++w) {  // stable LSD: id, seq, time, [rank desc]
             big_gather_key<<<grid, threads, 0, s>>>(bt, vals_a, keys_a, w);
+            const int end_bit = w == 0 ? static_cast<int>(8 * id_bytes) : w == 1 ? static_cast<int>(8 * seq_bytes) : 64;
             cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
-                                            static_cast<int>(np), 0, 64, s);
+                                            static_cast<int>(np), 0, end_bit, s);
             std::swap(vals_a, vals_b);
         }
         big_ord<<<grid, threads, 0, s>>>(np, vals_a, ord);
