@@ -47,6 +47,7 @@ struct BigReq {  // lives in device memory (part of the uploaded blob): the grap
     uint64_t cpu_used, cpu_cap;
     int32_t wa, offload, has_floor;
     uint64_t bpt;  // bytes per token (per call: not baked into the graph)
+    int64_t rank_max;  // rank_bytes < 8: every rank is SUFFIX, UNREACHABLE or in [0, rank_max]
 };
 
 __device__ __forceinline__ uint64_t time_order(double t) {
@@ -70,7 +71,17 @@ __global__ void big_stage(BigTree t, const BigReq* __restrict__ q, uint8_t* flag
 // keys[k] = word `w` of node vals[k]'s `before` key (ascending = earlier).  Only the relative
 // order of candidates matters downstream (ord is read for R nodes only), so non-candidates
 // need no extra pass to sort last.
-__global__ void big_gather_key(BigTree t, const uint32_t* vals, uint64_t* keys, int w) {
+// WA rank word, descending.  Compact form (rank_bytes < 8, decided on the host): SUFFIX -> 0,
+// UNREACHABLE -> 1, r in [0, rank_max] -> 2 + rank_max - r -- the same order in a few bytes.
+__device__ __forceinline__ uint64_t rank_key(int64_t r, const BigReq* q, bool compact) {
+    if (!compact) return ~(static_cast<uint64_t>(r) ^ 0x8000000000000000ull);
+    if (r == kSuffix) return 0;
+    if (r == kUnreach) return 1;
+    return 2 + static_cast<uint64_t>(q->rank_max - r);
+}
+
+__global__ void big_gather_key(BigTree t, const BigReq* q, const uint32_t* vals, uint64_t* keys, int w,
+                               bool compact_rank) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
         const uint32_t i = vals[k];
         uint64_t key;
@@ -78,7 +89,7 @@ __global__ void big_gather_key(BigTree t, const uint32_t* vals, uint64_t* keys, 
             case 0: key = t.id[i]; break;
             case 1: key = t.seq[i]; break;
             case 2: key = time_order(t.time[i]); break;
-            default: key = ~(static_cast<uint64_t>(t.rank[i]) ^ 0x8000000000000000ull); break;  // rank desc
+            default: key = rank_key(t.rank[i], q, compact_rank); break;  // rank desc
         }
         keys[k] = key;
     }
@@ -263,10 +274,28 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
         return b;
     };
     const uint32_t id_bytes = live_bytes(max_id), seq_bytes = live_bytes(max_seq);
-    const uint64_t key = (static_cast<uint64_t>(np) << 9) | (id_bytes << 5) | (seq_bytes << 1) | (wa ? 1u : 0u);
+    // WA: ranks are SUFFIX, UNREACHABLE or small step ranks (radix_cache.hpp:30-38) -> a compact
+    // order-preserving code (rank_key); anything else keeps the full 64-bit word
+    uint32_t rank_bytes = 8;
+    if (wa) {
+        int64_t rmax = 0;
+        bool small = true;
+        for (uint32_t i = 0; i < n && small; ++i) {
+            const int64_t r = t->rank[i];
+            if (r == kSuffix || r == kUnreach) continue;
+            if (r < 0 || r > (int64_t{1} << 40)) small = false;
+            else rmax = std::max(rmax, r);
+        }
+        if (small) {
+            rank_bytes = live_bytes(static_cast<uint64_t>(rmax) + 2);
+            hreq->rank_max = rmax;
+        }
+    }
+    const uint64_t key = (static_cast<uint64_t>(np) << 13) | (rank_bytes << 9) | (id_bytes << 5) | (seq_bytes << 1) |
+                         (wa ? 1u : 0u);
     auto git = e->big_graphs.find(key);
     if (git == e->big_graphs.end()) {
-        // ---- capture the whole device-wide sequence once per (bucket, policy, id / seq widths) ----
+        // ---- capture the whole device-wide sequence once per (bucket, policy, key widths) ----
         char* d = static_cast<char*>(e->ws_big.dev);
         char* dp = d;
         const BigReq* dreq = take<BigReq>(dp, 1);
@@ -303,8 +332,11 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
         cudaMemsetAsync(d_hdr, 0, 32, s);
         big_stage<<<grid, threads, 0, s>>>(bt, dreq, flags, blocked, vals_a);
         for (int w = 0; w < (wa ? 4 : 3); ++w) {  // stable LSD: id, seq, time, [rank desc]
-            big_gather_key<<<grid, threads, 0, s>>>(bt, vals_a, keys_a, w);
-            const int end_bit = w == 0 ? static_cast<int>(8 * id_bytes) : w == 1 ? static_cast<int>(8 * seq_bytes) : 64;
+            big_gather_key<<<grid, threads, 0, s>>>(bt, dreq, vals_a, keys_a, w, rank_bytes < 8);
+            const int end_bit = w == 0   ? static_cast<int>(8 * id_bytes)
+                                : w == 1 ? static_cast<int>(8 * seq_bytes)
+                                : w == 3 ? static_cast<int>(8 * rank_bytes)
+                                         : 64;
             cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
                                             static_cast<int>(np), 0, end_bit, s);
             std::swap(vals_a, vals_b);
