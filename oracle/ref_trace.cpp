@@ -458,11 +458,16 @@ int run_prio(const std::map<std::string, std::string>& kv) {
     std::mt19937_64 rng(getu(kv, "seed", 11));
     size_t cases = getu(kv, "cases", 100);
     size_t max_nodes = getu(kv, "max_nodes", 200);
+    // optional (the default stream of random draws, and so every golden vector, is unchanged):
+    // min_nodes / agents override the drawn sizes, time=1 adds the call's steady_clock time
+    const size_t min_nodes = getu(kv, "min_nodes", 0), agents_fixed = getu(kv, "agents", 0);
+    const bool timed = getu(kv, "time", 0) != 0;
     for (size_t c = 0; c < cases; ++c) {
         Scenario sc(16, 0);
         VirtualTime now = 0;
-        grow(sc, rng, 1 + rng() % max_nodes, static_cast<int>(3 + rng() % 6), now);
+        grow(sc, rng, std::max<size_t>(min_nodes, 1 + rng() % max_nodes), static_cast<int>(3 + rng() % 6), now);
         size_t agents = 1 + rng() % 12;
+        if (agents_fixed) agents = agents_fixed;
         std::vector<AgentId> ids;
         for (size_t a = 0; a < agents; ++a) {
             AgentId id{static_cast<ClientId>(rng() % 3), "p" + std::to_string(a)};
@@ -476,9 +481,12 @@ int run_prio(const std::map<std::string, std::string>& kv) {
             if (r < 7) steps[id] = static_cast<StepValue>(rng() % 9);
             else if (r == 7) steps[id] = kStepUnreachable;
         }
+        const auto t0 = std::chrono::steady_clock::now();
         sc.cache.set_agent_priorities(steps);
+        const double prio_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
         Snapshot snap = snapshot(sc.cache);
         std::printf("{\"t\":\"prio\",\"case\":%zu,", c);
+        if (timed) std::printf("\"prio_us\":%.3f,", prio_us);
         print_tree(sc.cache, snap);
         // boundary agents (node index, candidate rank) in map order of the agent id
         std::map<AgentId, int> bidx;

@@ -90,7 +90,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* parent, uint32_t n, const int32_t* bidx,
                                                                 const int64_t* cand, uint32_t m, long long* out,
                                                                 const uint8_t* blob, uint32_t blob_bytes,
-                                                                unsigned long long* hdr, unsigned long long seq) {
+                                                                unsigned long long* hdr, unsigned long long seq,
+                                                                long long* scratch) {
     extern __shared__ __align__(16) uint8_t psm[];
     const unsigned long long t_begin = gtimer();
     const bool staged = n <= kPrioSmemNodes;
@@ -102,16 +103,18 @@ __global__ void __launch_bounds__(kThreads) kvf_priority_kernel(const int32_t* p
         bidx = rebase(bidx, blob, sb);
         cand = rebase(cand, blob, sb);
     }
-    long long* r = staged ? rank : out;
+    // ranks beyond shared memory accumulate in device scratch when `out` is mapped host memory
+    // (atomics there would cross PCIe one by one), else in `out` itself
+    long long* r = staged ? rank : (scratch ? scratch : out);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = kRankSuffix;
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
         const long long c = cand[b];
         for (int32_t v = bidx[b]; v > 0; v = parent[v]) atomicMin(r + v, c);
     }
-    if (staged) {
+    if (r != out) {
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = rank[i];
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = r[i];
     }
     if (hdr && threadIdx.x == 0) {
         hdr[3] = t_begin;
@@ -735,7 +738,10 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     const uint32_t prio_threads = std::min<uint32_t>(kThreads, std::max<uint32_t>(128, pow2_ceil(std::max(n, m))));
     kvf_priority_kernel<<<1, prio_threads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
                                                          zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
-                                                         zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq);
+                                                         zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq,
+                                                         zero_copy && n > kPrioSmemNodes
+                                                             ? static_cast<long long*>(e->ws_dec.dev)
+                                                             : nullptr);
     KVF_CUDA(cudaGetLastError());
     if (decision_trace_path()) tr.t_launched = std::chrono::steady_clock::now();
     e->stats.kernel_launches++;
