@@ -704,26 +704,30 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     std::memcpy(carve<int64_t>(hp, m), cand, m * 8);
     const size_t used = static_cast<size_t>(hp - h);
     const size_t out_off = (used + 255) & ~size_t(255);
-    // Small trees: the kernel reads its inputs from, and writes its result to, mapped pinned
-    // memory -- one launch + one sync, no memcpy launches.  Large: classic H2D / D2H.
-    const bool zero_copy = in_bytes <= kZeroCopyBytes;
-    char* base = zero_copy ? static_cast<char*>(e->ws_dec.host_dev) : static_cast<char*>(e->ws_dec.dev);
+    // The result (ranks, stamps, done word) always goes to mapped pinned memory -- coalesced
+    // posted writes, the host spins on the done word: no D2H copy, no stream sync.  Inputs up
+    // to kZeroCopyBytes are read in place from mapped memory too (one launch in all); larger
+    // ones take one H2D copy ahead of the kernel on the same stream.
+    const bool zero_in = in_bytes <= kZeroCopyBytes;
+    char* hdev = static_cast<char*>(e->ws_dec.host_dev);
+    char* ddev = static_cast<char*>(e->ws_dec.dev);
+    char* base = zero_in ? hdev : ddev;
     char* dp = base;
     int32_t* d_parent = carve<int32_t>(dp, n);
     int32_t* d_bidx = carve<int32_t>(dp, m);
     int64_t* d_cand = carve<int64_t>(dp, m);
-    long long* d_out = reinterpret_cast<long long*>(base + out_off);
-    // header (stamps + done word) after the ranks, in mapped memory on the fast path
+    long long* d_out = reinterpret_cast<long long*>(hdev + out_off);
+    // ranks beyond shared memory accumulate in device scratch (never atomics on mapped memory)
+    long long* scratch = n > kPrioSmemNodes ? reinterpret_cast<long long*>(ddev + out_off) : nullptr;
     const size_t hdr_off = (out_off + n * 8 + 255) & ~size_t(255);
     unsigned long long* h_hdr = reinterpret_cast<unsigned long long*>(h + hdr_off);
-    unsigned long long* d_hdr = zero_copy ? reinterpret_cast<unsigned long long*>(base + hdr_off) : nullptr;
+    unsigned long long* d_hdr = reinterpret_cast<unsigned long long*>(hdev + hdr_off);
     const unsigned long long seq = ++e->dec_seq;
     // the done word sits wherever this call's n puts it -- possibly on bytes an earlier call
     // left there (victim indices can equal a sequence number): clear it before the launch
-    if (zero_copy) __atomic_store_n(h_hdr + kDoneWord, 0ull, __ATOMIC_RELEASE);
-    if (!zero_copy) KVF_CUDA(cudaMemcpyAsync(base, h, used, cudaMemcpyHostToDevice, e->s_dec));
-    if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
-    const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_copy ? used : 0);
+    __atomic_store_n(h_hdr + kDoneWord, 0ull, __ATOMIC_RELEASE);
+    if (!zero_in) KVF_CUDA(cudaMemcpyAsync(ddev, h, used, cudaMemcpyHostToDevice, e->s_dec));
+    const size_t smem = (n <= kPrioSmemNodes ? (n * 8ull + 15) & ~15ull : 0) + (zero_in ? used : 0);
     if (!e->prio_attr_set) {
         KVF_CUDA(cudaFuncSetAttribute(kvf_priority_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kPrioSmemNodes * 8 + kZeroCopyBytes + 64)));
@@ -737,25 +741,16 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
     // sized to the tree (128..1024 threads): a small CTA also fits beside a K6 CTA on a busy SM
     const uint32_t prio_threads = std::min<uint32_t>(kThreads, std::max<uint32_t>(128, pow2_ceil(std::max(n, m))));
     kvf_priority_kernel<<<1, prio_threads, smem, e->s_dec>>>(d_parent, n, d_bidx, d_cand, m, d_out,
-                                                         zero_copy ? reinterpret_cast<const uint8_t*>(base) : nullptr,
-                                                         zero_copy ? static_cast<uint32_t>(used) : 0u, d_hdr, seq,
-                                                         zero_copy && n > kPrioSmemNodes
-                                                             ? static_cast<long long*>(e->ws_dec.dev)
-                                                             : nullptr);
+                                                         zero_in ? reinterpret_cast<const uint8_t*>(base) : nullptr,
+                                                         zero_in ? static_cast<uint32_t>(used) : 0u, d_hdr, seq,
+                                                         scratch);
     KVF_CUDA(cudaGetLastError());
     if (decision_trace_path()) tr.t_launched = std::chrono::steady_clock::now();
     e->stats.kernel_launches++;
     e->stats.decisions++;
-    if (zero_copy) {
-        if (int src = spin_decision(e, h_hdr, seq, t0, &tr, "k4", n)) return src;
-        std::memcpy(out_rank, h + out_off, n * 8);
-        return KVF_OK;
-    }
-    KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
-    KVF_CUDA(cudaMemcpyAsync(h + out_off, d_out, n * 8, cudaMemcpyDeviceToHost, e->s_dec));
-    KVF_CUDA(cudaStreamSynchronize(e->s_dec));
+    if (int src = spin_decision(e, h_hdr, seq, t0, &tr, "k4", n)) return src;
     std::memcpy(out_rank, h + out_off, n * 8);
-    return finish_decision(e, t0);
+    return KVF_OK;
 }
 
 int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
