@@ -37,7 +37,6 @@ constexpr int64_t kRankSuffix = INT64_MAX / 2;        // radix_cache.hpp:30-38
 constexpr int64_t kRankUnreachable = INT64_MAX / 4;
 constexpr uint32_t kMaxNodesSingleCta = 4096;
 constexpr int kThreads = 1024;
-constexpr int32_t kBlocked = INT32_MAX;
 // K5 result header: [count, immediate, pending, 6 globaltimer stamps, 6 clock64 stamps, done seq]
 constexpr size_t kHeaderBytes = 128;
 constexpr int kDoneWord = 15;  // the host spins on header[15] == call sequence number
@@ -788,7 +787,10 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     std::memcpy(carve<uint8_t>(hp, n), t->status, n);
     std::memcpy(carve<uint8_t>(hp, n), t->backed, n);
     const size_t used = static_cast<size_t>(hp - h);
-    const bool zero_copy = used <= kZeroCopyBytes;  // read in place from mapped pinned memory
+    // inputs up to kZeroCopyBytes are read in place from mapped pinned memory, larger ones take
+    // one H2D copy ahead of the kernel; the result always goes to mapped memory (posted
+    // writes) and the host spins on its done word -- no D2H copy, no stream sync
+    const bool zero_copy = used <= kZeroCopyBytes;
     char* d = zero_copy ? static_cast<char*>(e->ws_dec.host_dev) : static_cast<char*>(e->ws_dec.dev);
     char* dp = d;
     TreeDev td;
@@ -806,7 +808,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     td.bpt = t->bytes_per_token;
     td.blob = zero_copy ? reinterpret_cast<const uint8_t*>(d) : nullptr;
     td.blob_bytes = zero_copy ? static_cast<uint32_t>(used) : 0u;
-    char* dout = d + ((used + 255) & ~size_t(255));
+    char* dout = static_cast<char*>(e->ws_dec.host_dev) + ((used + 255) & ~size_t(255));
     OutDev od;
     od.header = reinterpret_cast<unsigned long long*>(dout);
     od.idx = reinterpret_cast<int32_t*>(dout + kHeaderBytes);
@@ -820,12 +822,11 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
                                       static_cast<int>(victim_smem(kMaxNodesSingleCta))));
         e->victim_attr_set = true;
     }
-    od.spin = zero_copy;
+    od.spin = true;
     const unsigned long long seq = ++e->dec_seq;
-    if (zero_copy)  // see kvf_priority_propagate: never spin on a stale word
-        __atomic_store_n(reinterpret_cast<unsigned long long*>(h + ((used + 255) & ~size_t(255))) + kDoneWord, 0ull,
-                         __ATOMIC_RELEASE);
-    if (!zero_copy) KVF_CUDA(cudaEventRecord(e->dec_start, e->s_dec));
+    // see kvf_priority_propagate: never spin on a stale word
+    __atomic_store_n(reinterpret_cast<unsigned long long*>(h + ((used + 255) & ~size_t(255))) + kDoneWord, 0ull,
+                     __ATOMIC_RELEASE);
     DecisionTrace tr;
     if (decision_trace_path()) {
         tr.t_launch = std::chrono::steady_clock::now();
@@ -840,14 +841,8 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     e->stats.kernel_launches++;
     e->stats.decisions++;
     char* hout = h + ((used + 255) & ~size_t(255));
-    if (zero_copy) {
-        if (int src = spin_decision(e, reinterpret_cast<const unsigned long long*>(hout), seq, t0, &tr, "k5", n))
-            return src;
-    } else {
-        KVF_CUDA(cudaEventRecord(e->dec_stop, e->s_dec));
-        KVF_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, e->s_dec));
-        KVF_CUDA(cudaStreamSynchronize(e->s_dec));
-    }
+    if (int src = spin_decision(e, reinterpret_cast<const unsigned long long*>(hout), seq, t0, &tr, "k5", n))
+        return src;
     const uint64_t* hdr = reinterpret_cast<const uint64_t*>(hout);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
     for (int k = 0; k < 5; ++k) {
@@ -859,7 +854,7 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
     *out_count = cnt;
     *out_imm = hdr[1];
     *out_pend = hdr[2];
-    return zero_copy ? KVF_OK : finish_decision(e, t0);
+    return KVF_OK;
 }
 
 }  // extern "C"
