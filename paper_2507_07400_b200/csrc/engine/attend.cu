@@ -776,3 +776,14 @@ extern "C" int kvf_decode_attend_layers(kvf_engine* e, uint64_t job_id, uint32_t
     KVF_GUARD(e);
     return attend_impl(e, job_id, layer0, nlayers, batch, group, q, runs, run_counts, scale, out, chunk_tokens);
 }
+
+namespace kvf_impl {
+void set_carveout_attend() {
+    cudaFuncSetAttribute(kvf_attend_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kvf_attend_combine_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kvf_attend_zero_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+}
+}  // namespace kvf_impl

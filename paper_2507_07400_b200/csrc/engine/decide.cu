@@ -858,3 +858,12 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_req
 }
 
 }  // extern "C"
+
+namespace kvf_impl {
+void set_carveout_decide() {
+    cudaFuncSetAttribute(kvf_priority_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(kvf_victim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+}
+}  // namespace kvf_impl

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "engine_internal.hpp"
@@ -692,6 +693,20 @@ uint32_t grid_short(uint64_t work, uint32_t threads, uint32_t per_thread) {
     return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(g, 0x7fffffffull)));
 }
 
+void set_carveout_engine() {
+    const int v = cudaSharedmemCarveoutMaxShared;
+    const cudaFuncAttribute a = cudaFuncAttributePreferredSharedMemoryCarveout;
+    cudaFuncSetAttribute(kvf_copy_vec_kernel<uint4, 4>, a, v);
+    cudaFuncSetAttribute(kvf_copy_vec_kernel<uint4, 8>, a, v);
+    cudaFuncSetAttribute(kvf_copy_vec_kernel<uint2, 8>, a, v);
+    cudaFuncSetAttribute(kvf_copy_bulk_kernel<kBulkStages, kBulkChunk>, a, v);
+    cudaFuncSetAttribute(kvf_wait_layer_kernel, a, v);
+    cudaFuncSetAttribute(kvf_spin_kernel, a, v);
+    cudaFuncSetAttribute(kvf_fill_kernel, a, v);
+    cudaFuncSetAttribute(kvf_checksum_kernel, a, v);
+    cudaFuncSetAttribute(kvf_payload_checksum_kernel, a, v);
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -815,6 +830,13 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
     for (int32_t k = static_cast<int32_t>(kvf_impl::kLayerSlots) - 1; k >= 0; --k) e->lr_free.push_back(k);
     // Size the staging workspaces once: growing them later means cudaFree (a device-wide
     // sync) and cudaHostAlloc inside a decision call -- milliseconds on the hot path.
+    static std::once_flag carveout_once;  // attributes are per function (all devices alike here)
+    std::call_once(carveout_once, [] {
+        set_carveout_engine();
+        kvf_impl::set_carveout_decide();
+        kvf_impl::set_carveout_attend();
+    });
+    cudaGetLastError();  // an attribute a driver rejects is a hint, not an error
     if (int rc = e->ws_dec.ensure(1u << 20, 1u << 20)) return fail(rc);
     if (int rc = e->ws_dev.ensure(4u << 20, 4u << 20)) return fail(rc);
     *out = e;

@@ -146,6 +146,12 @@ int acquire_event(kvf_engine* e, cudaEvent_t* ev);
 int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j);
 int end_job(kvf_engine* e, uint64_t job_id, Job& j);
 void clear_stale_error(kvf_engine* e, const char* fn);
+// Every engine kernel prefers the max-shared-memory carveout, so SMs never switch their L1 /
+// shared split between kernels: a switch needs a drained SM, and a streaming grid (a prompt
+// fill) keeps every SM busy until it ends -- a decision CTA needing a different split waited
+// ~0.6 ms for that (scripts/decision_trace.py, KVF_ARRIVAL_TRACE).  Once per process.
+void set_carveout_decide();
+void set_carveout_attend();
 int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
                         uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend);
 void recycle_event(kvf_engine* e, cudaEvent_t ev);
