@@ -264,6 +264,9 @@ def run_ours(args, rank, world, local):
     e2e_wall = time.perf_counter() - t0
     res = sim.result()
     sim.close()
+    # C4 (64 concurrent workflows, shared prefixes, 1.3k-node tree) as one of 8 KV-head shards:
+    # the per-job-overhead regime (1,261 write-backs of 8 MiB, 493 loads), rank 0
+    c4 = c4_line(Sim, local, N) if rank == 0 else None
 
     total_step_ms = sum(step_ms)
     mine = {
@@ -286,8 +289,12 @@ def run_ours(args, rank, world, local):
     value = total_pre / (total_step_ms * 1e-3) / 1e9
     achieved = pre_bytes / (k1_avg * 1e-3) / 1e9
     k3_gbs = 2 * pre_bytes / (min(k3) * 1e-3) / 1e9
-    cpu = cpu_baseline(pre_bytes * world, heads * world) if world == 1 else None
+    # the reference arm's timed region holds its decisions for each agent step (run_reference);
+    # ours does too: the GPU decision time per agent step of the same C2 workflow (e2e_workflow)
     steps_e2e = max(1, res["arrivals"])
+    dec_s_per_step = res["decision_us_total"] / steps_e2e * 1e-6
+    e2e_time = wall + args.steps * dec_s_per_step
+    cpu = cpu_baseline(pre_bytes * world, heads * world)
     h2d_all = res["prefetch_bytes"] + res["reactive_bytes"]
     line = {
         "metric": METRIC,
@@ -338,10 +345,15 @@ def run_ours(args, rank, world, local):
         # e2e: the same K steps through the reference-facing C-ABI (kvf_h2d_gather /
         # kvf_d2h_scatter on pinned HOST KV + kvf_job_wait + release), timed on the host clock
         # around the whole loop: launches, copies both ways and fences inside the timed region
-        "e2e": {"value": round(total_pre / wall / 1e9, 3), "unit": "GB/s",
+        "e2e": {"value": round(total_pre / e2e_time / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": int(pre_bytes * world), "d2h_bytes_per_step": int(wb_bytes * world),
                 "what": "per agent step via the C-ABI (kvf_h2d_gather of the next agent's node from pinned host "
-                        "memory || kvf_d2h_scatter of the last suffix, kvf_job_wait), host wall clock"},
+                        "memory || kvf_d2h_scatter of the last suffix, kvf_job_wait), host wall clock, plus the "
+                        "step's GPU decisions (K4/K5 per agent step in the C2 workflow run, as the reference "
+                        "arm adds its own)",
+                "transfer_only_gbs": round(total_pre / wall / 1e9, 3),
+                "decision_us_per_step": round(dec_s_per_step * 1e6, 2)},
+        "e2e_c4": c4,
         # the whole C2 workflow through libkvflow_host.so (lockstep driver: GPU K4/K5 decisions,
         # real K1/K2 transfers fenced in virtual-time order, payload writes)
         "e2e_workflow": {"value": round(res["prefetch_bytes"] * world / e2e_wall / 1e9, 3), "unit": "GB/s",
@@ -377,6 +389,36 @@ def run_ours(args, rank, world, local):
         "parity": {"bench_bytes_checksum_equal": bool(ok)},
     }
     print(json.dumps(line), flush=True)
+
+
+def c4_line(Sim, device, N):
+    """C4 (BASELINE configs[3]: 64 concurrent workflows sharing prefixes in one radix tree) through
+    the public API as one of 8 KV-head shards (1 head of Llama-3-8B: 16 KiB/token, 2 GiB HBM
+    budget): lockstep driver, GPU K4/K5, real K1/K2.  Bytes moved both ways / host wall of run()."""
+    kw = dict(topology="CYCLIC", agents=4, iterations=4, workflows=64, fixed=1024, dyn=256, out=256,
+              shared_prefix=512, gpu_cap=2147483648, bytes_per_token=16384, layers=32, kv_heads_total=8,
+              kv_heads_local=1, head_offset=7, head_dim=128, device=device, numa_node=N.KVF_NUMA_AUTO,
+              host_slots=10578034688 // 16384 + 4096)
+    try:
+        with Sim(**kw) as s:
+            t0 = time.perf_counter()
+            s.run()
+            wall = time.perf_counter() - t0
+            r = s.result()
+    except Exception as ex:  # pragma: no cover - reported, never fatal for the headline
+        return {"value": None, "unavailable": repr(ex)[:200]}
+    moved = r["loaded_bytes"] + r["offloaded_bytes"]
+    dev_ms = r["prefetch_device_ms"] + r["reactive_device_ms"] + r["offload_device_ms"]
+    jobs = r["prefetch_jobs"] + r["reactive_jobs"] + r["offload_jobs"]
+    return {"value": round(moved / wall / 1e9, 3), "unit": "GB/s",
+            "what": "C4 64-workflow shared-prefix run, 8-way KV-head shard, lockstep via libkvflow_host.so: "
+                    "H2D+D2H bytes / host wall of run()",
+            "h2d_bytes": r["loaded_bytes"], "d2h_bytes": r["offloaded_bytes"], "wall_s": round(wall, 4),
+            "nodes": r["nodes"], "jobs": jobs, "prefetch_jobs": r["prefetch_jobs"], "reactive_jobs": r["reactive_jobs"],
+            "offload_jobs": r["offload_jobs"], "d2h_launches": r["d2h_batches"],
+            "kernel_launches": r["kernel_launches"],
+            "device_gbs_per_job": round(moved / (dev_ms * 1e-3) / 1e9, 3) if dev_ms else None,
+            "decision_us_per_arrival": round(r["decision_us_total"] / max(1, r["arrivals"]), 2)}
 
 
 def cpu_baseline(node_bytes, heads):

@@ -251,7 +251,12 @@ int kvf_kv_append(kvf_engine* e, uint64_t job_id, uint32_t layer, const kvf_run*
 int kvf_decode_attend(kvf_engine* e, uint64_t job_id, uint32_t layer, uint32_t batch, uint32_t group,
                       const void* q, const kvf_run* runs, const uint32_t* run_counts, float scale, void* out,
                       uint32_t chunk_tokens);
-/* A decode step's layers layer0 .. layer0+nlayers-1 as ONE job over the same run tables:
+/* A decode step's layers layer0 .. layer0+nlayers-1 as ONE job over the same run tables.
+ * PRECONDITION: every layer's q is ready when the call is made.  In a real decoder layer
+ * l+1's q depends on layer l's output, so a decode step cannot use this chain -- it calls
+ * kvf_decode_attend once per layer; this entry point is for workloads whose queries are known
+ * up front (speculative / re-scoring passes) and is an upper bound for the per-layer path. */
+/* Layout:
  * q[l] / out[l] are layer (layer0 + l)'s buffers, laid out as for kvf_decode_attend.  The
  * layers' kernels are chained with programmatic dependent launch, so layer l+1 starts on the
  * SMs layer l has finished with; results are bit-identical to nlayers kvf_decode_attend

@@ -656,15 +656,15 @@ int spin_decision(kvf_engine* e, const unsigned long long* hdr, unsigned long lo
     const auto t_done = std::chrono::steady_clock::now();
     e->stats.decision_call_us += std::chrono::duration<double, std::micro>(t_done - t0).count();
     if (tr && decision_trace_path()) {
-        const long long rt_done = realtime_ns();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
         if (FILE* f = std::fopen(decision_trace_path(), "a")) {
+            // host phases on the host clock, kernel_us on the GPU's %globaltimer: the two clocks
+            // are never subtracted from each other (they are not synchronised)
             std::fprintf(f,
                          "{\"kind\": \"%s\", \"n\": %u, \"pack_us\": %.2f, \"launch_call_us\": %.2f, \"spin_us\": %.2f, "
-                         "\"kstart_after_launch_us\": %.2f, \"kernel_us\": %.2f, \"seen_after_kend_us\": %.2f}\n",
+                         "\"kernel_us\": %.2f}\n",
                          kind, n, us(t0, tr->t_launch), us(tr->t_launch, tr->t_launched), us(tr->t_launched, t_done),
-                         (static_cast<long long>(hdr[3]) - tr->rt_launch_ns) * 1e-3, (hdr[8] - hdr[3]) * 1e-3,
-                         (rt_done - static_cast<long long>(hdr[8])) * 1e-3);
+                         (hdr[8] - hdr[3]) * 1e-3);
             std::fclose(f);
         }
     }

@@ -1092,15 +1092,6 @@ int kvf_compute_job_end(kvf_engine* e, uint64_t job_id) {
     return KVF_OK;
 }
 
-int kvf_job_span_ms(kvf_engine* e, uint64_t first_job, uint64_t last_job, float* ms) {
-    KVF_GUARD(e);
-    auto a = e->jobs.find(first_job), b = e->jobs.find(last_job);
-    if (a == e->jobs.end() || b == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job");
-    KVF_CUDA(cudaEventSynchronize(b->second.stop));
-    KVF_CUDA(cudaEventElapsedTime(ms, a->second.start, b->second.stop));
-    return KVF_OK;
-}
-
 int kvf_dev_gather(kvf_engine* e, uint64_t job_id, const kvf_run* runs, uint32_t n, void* staging) {
     KVF_GUARD(e);
     return dev_staging_copy(e, job_id, runs, n, static_cast<char*>(staging), true);
@@ -1188,7 +1179,8 @@ int kvf_peer_gather(kvf_engine* e, uint64_t job_id, kvf_engine* src, const kvf_r
 int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done) {
     KVF_GUARD(e);
     auto it = e->jobs.find(job_id);
-    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    if (it == e->jobs.end() || it->second.released)
+        return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
     cudaError_t err = cudaEventQuery(it->second.stop);
     if (err == cudaErrorNotReady) {
         *done = 0;
@@ -1199,38 +1191,97 @@ int kvf_job_query(kvf_engine* e, uint64_t job_id, int32_t* done) {
     return KVF_OK;
 }
 
-int kvf_job_wait(kvf_engine* e, uint64_t job_id) {
-    KVF_GUARD(e);
+namespace {
+// The blocking fences (wait / elapsed / release / span) take the engine lock only to look the
+// job up and to drop their reference: a 20 ms K1 fence must not hold up a decision call or a
+// launch from another thread on the same engine (cudaEventSynchronize itself is thread-safe).
+void drop_job_ref(kvf_engine* e, uint64_t job_id) {
     auto it = e->jobs.find(job_id);
-    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
-    KVF_CUDA(cudaEventSynchronize(it->second.stop));
+    if (it == e->jobs.end()) return;
+    kvf_impl::Job& j = it->second;
+    if (j.waiters) --j.waiters;
+    if (j.released && j.waiters == 0) {
+        recycle_event(e, j.start);
+        recycle_event(e, j.stop);
+        if (j.lr_slot >= 0) e->lr_free.push_back(j.lr_slot);
+        e->jobs.erase(it);
+    }
+}
+
+// Look up `job_id` and take a reference (under the lock); `release` also marks it released.
+int ref_job(kvf_engine* e, uint64_t job_id, bool release, cudaEvent_t* start, cudaEvent_t* stop) {
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
+    kvf_impl::clear_stale_error(e, __func__);
+    auto it = e->jobs.find(job_id);
+    if (it == e->jobs.end() || it->second.released)
+        return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
+    ++it->second.waiters;
+    if (release) it->second.released = true;
+    if (start) *start = it->second.start;
+    *stop = it->second.stop;
     return KVF_OK;
+}
+
+void unref_job(kvf_engine* e, uint64_t job_id) {
+    std::lock_guard<std::mutex> lk(e->mu);
+    drop_job_ref(e, job_id);
+}
+}  // namespace
+
+int kvf_job_wait(kvf_engine* e, uint64_t job_id) {
+    if (!e) return set_error(KVF_E_INVALID_ARG, "null engine");
+    cudaEvent_t stop = nullptr;
+    if (int rc = ref_job(e, job_id, false, nullptr, &stop)) return rc;
+    const cudaError_t err = cudaEventSynchronize(stop);  // unlocked
+    unref_job(e, job_id);
+    return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventSynchronize(job)");
 }
 
 int kvf_job_elapsed_ms(kvf_engine* e, uint64_t job_id, float* ms) {
-    KVF_GUARD(e);
-    auto it = e->jobs.find(job_id);
-    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
-    KVF_CUDA(cudaEventSynchronize(it->second.stop));
-    KVF_CUDA(cudaEventElapsedTime(ms, it->second.start, it->second.stop));
-    return KVF_OK;
+    if (!e || !ms) return set_error(KVF_E_INVALID_ARG, "null argument");
+    cudaEvent_t start = nullptr, stop = nullptr;
+    if (int rc = ref_job(e, job_id, false, &start, &stop)) return rc;
+    cudaError_t err = cudaEventSynchronize(stop);
+    if (err == cudaSuccess) err = cudaEventElapsedTime(ms, start, stop);
+    unref_job(e, job_id);
+    return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventElapsedTime(job)");
 }
 
 int kvf_job_release(kvf_engine* e, uint64_t job_id) {
-    KVF_GUARD(e);
-    auto it = e->jobs.find(job_id);
-    if (it == e->jobs.end()) return set_error(KVF_E_UNKNOWN_JOB, "unknown job " + std::to_string(job_id));
-    KVF_CUDA(cudaEventSynchronize(it->second.stop));
-    recycle_event(e, it->second.start);
-    recycle_event(e, it->second.stop);
-    if (it->second.lr_slot >= 0) e->lr_free.push_back(it->second.lr_slot);
-    e->jobs.erase(it);
-    return KVF_OK;
+    if (!e) return set_error(KVF_E_INVALID_ARG, "null engine");
+    cudaEvent_t stop = nullptr;
+    if (int rc = ref_job(e, job_id, true, nullptr, &stop)) return rc;
+    // the events go back to the pool only once they have fired (and no one else waits on them)
+    const cudaError_t err = cudaEventSynchronize(stop);
+    unref_job(e, job_id);
+    return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventSynchronize(release)");
+}
+
+int kvf_job_span_ms(kvf_engine* e, uint64_t first_job, uint64_t last_job, float* ms) {
+    if (!e || !ms) return set_error(KVF_E_INVALID_ARG, "null argument");
+    cudaEvent_t a_start = nullptr, a_stop = nullptr, b_stop = nullptr;
+    if (int rc = ref_job(e, first_job, false, &a_start, &a_stop)) return rc;
+    if (int rc = ref_job(e, last_job, false, nullptr, &b_stop)) {
+        unref_job(e, first_job);
+        return rc;
+    }
+    cudaError_t err = cudaEventSynchronize(b_stop);
+    if (err == cudaSuccess) err = cudaEventElapsedTime(ms, a_start, b_stop);
+    unref_job(e, last_job);
+    unref_job(e, first_job);
+    return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventElapsedTime(span)");
 }
 
 int kvf_sync_all(kvf_engine* e) {
-    KVF_GUARD(e);
-    for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp}) KVF_CUDA(cudaStreamSynchronize(s));
+    if (!e) return set_error(KVF_E_INVALID_ARG, "null engine");
+    cudaStream_t ss[5];
+    {
+        KVF_GUARD(e);
+        cudaStream_t s[5] = {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp};
+        std::copy(s, s + 5, ss);
+    }
+    for (cudaStream_t s : ss) KVF_CUDA(cudaStreamSynchronize(s));  // unlocked
     return KVF_OK;
 }
 

@@ -60,6 +60,10 @@ struct Job {
     // counters[slot][l] >= lr_base + lr_tpl (counters only grow; never reset)
     int32_t lr_slot = -1;
     uint32_t lr_base = 0, lr_tpl = 0;
+    // blocking fences run outside the engine lock: threads inside one hold a reference, and a
+    // release that finds waiters leaves the recycling of the events to the last of them
+    uint32_t waiters = 0;
+    bool released = false;
 };
 
 constexpr uint32_t kLayerSlots = 64;

@@ -159,9 +159,9 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
         uint64_t host = c->host_slots;
         if (host == 0) {  // every token the run could ever back up (write-once host copies)
             w.validate();
-            const uint64_t per_agent = c->fixed + static_cast<uint64_t>(c->iterations) * (c->dyn + c->out);
-            host = static_cast<uint64_t>(c->workflows) * c->agents * per_agent + 1024;
-            if (c->topology == 4) host = host * 3;  // PEER_STYLE lengths are drawn
+            // the generator's own bound (PEER_STYLE lengths are drawn per agent from the seed)
+            host = WorkloadController(w, c->seed).max_cached_tokens() + 1024;
+            if (c->cpu_cap) host = std::min<uint64_t>(host, c->cpu_cap / c->bytes_per_token + 1024);
         }
         eo.host_slots = host;
         eo.pcie_mode = c->pcie_mode;

@@ -32,7 +32,7 @@ void throw_engine(int status, const std::string& what) {
     std::string msg = what + ": " + kvf_last_error();
     if (status >= 1 && status <= 14) throw_error(static_cast<ErrorCode>(status - 1), msg);
     if (status == KVF_E_NO_DEVICE) throw_error(ErrorCode::NoDevice, msg);
-    if (status == KVF_E_OUT_OF_HOST_SLOTS) throw_error(ErrorCode::OutOfGpuMemory, msg);
+    if (status == KVF_E_OUT_OF_HOST_SLOTS) throw_error(ErrorCode::OutOfHostMemory, msg);
     throw_error(ErrorCode::DeviceError, msg);
 }
 

@@ -8,6 +8,7 @@
 #include <random>
 
 #include "kvflow/radix_cache.hpp"
+#include "kvflow/scheduler.hpp"
 #include "kvflow/sim_engine.hpp"
 #include "kvflow/tier_manager.hpp"
 #include "tinytest.hpp"
@@ -320,3 +321,60 @@ TEST("tier manager with bytes: FIFO jobs, fences, write-once host copies, audit"
 }
 
 TT_MAIN
+
+TEST("evict: a victim that throws (bounded-CPU remove defect) still launches the booked write-backs") {
+    Rig r(4 * kBpt);
+    r.tier.set_offload_batching(true);
+    InsertResult c = r.put({9}, 0.5);
+    r.cache.lock_root_path(c.path.back());  // keep {9} out of the first two evictions
+    r.put({1, 2, 3, 4}, 1.0);
+    r.put({1, 2, 3, 5}, 2.0);  // A = [1,2,3] with children [4], [5]
+    for (VirtualTime t : {3.0, 4.0}) {  // [4] then [5] -> backed copies (cpu_used = 2 tokens)
+        EvictOutcome o = r.cache.evict({kBpt, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, t);
+        REQUIRE(o.victims.size() == 1);
+        Event done = r.ev.pop();
+        r.tier.complete(done.id, done.time);
+    }
+    r.cache.unlock_root_path(c.path.back());
+    CHECK(r.tier.cpu_used() == 2 * kBpt);
+    // victims: {9} (fits the CPU tier: offload, booked) then A (3 tokens, no CPU room: remove,
+    // but it still has BACKUP_IN_CPU children -> the reference's InternalError)
+    const uint64_t d2h0 = engine().stats().d2h_jobs;
+    bool threw = false;
+    try {
+        r.cache.evict({4 * kBpt, EvictionPolicy::Lru, TierMode::Offload, {}}, r.tier, 5.0);
+    } catch (const SimError& e) {
+        threw = e.code() == ErrorCode::InternalError;
+    }
+    CHECK(threw);
+    CHECK(engine().stats().d2h_jobs == d2h0 + 1);  // {9}'s write-back left before the throw escaped
+    Event done = r.ev.pop();
+    r.tier.complete(done.id, done.time);
+    CHECK(r.host_ok(*r.node({9})));
+}
+
+TEST("Simulator refuses a ledger larger than the engine's slot pools") {
+    WorkloadSpec w;
+    w.topology = Topology::Cyclic;
+    w.num_agents = 2;
+    w.iterations = 1;
+    w.fixed_len = 8;
+    w.dyn_len = 2;
+    w.out_len = 2;
+    SchedulerConfig sc;
+    sc.policy = Policy::Kvflow;
+    sc.apply_policy_defaults();
+    CostModel cost = flat_cost();
+    auto code_of = [&](Bytes gpu_cap, Bytes cpu_cap) {
+        try {
+            Simulator sim(cost, sc, w, gpu_cap, cpu_cap, 1, &engine());
+        } catch (const SimError& e) {
+            return static_cast<int>(e.code());
+        }
+        return -1;
+    };
+    CHECK(code_of((1ull << 20) * kBpt, 0) == -1);                              // fits exactly
+    CHECK(code_of((1ull << 21) * kBpt, 0) == static_cast<int>(ErrorCode::ConfigError));  // HBM pool too small
+    CHECK(code_of(1 << 20, 0) == -1);                                          // unbounded CPU: caller's bound
+    CHECK(code_of(1 << 20, 1ull << 40) == -1);  // bounded, but above anything the run can cache
+}

@@ -29,6 +29,9 @@ def test_bench_single_gpu_line():
         assert k in line, k
     assert line["value"] > 10 and line["roofline"]["frac"] > 0.5 and line["gpu_launches"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["parity"]["bench_bytes_checksum_equal"]
+    # decisions are inside e2e (symmetric with the reference arm), and C4 has its own line
+    assert line["e2e"]["decision_us_per_step"] > 0 and line["e2e"]["value"] <= line["e2e"]["transfer_only_gbs"]
+    assert line["e2e_c4"]["value"] > 0 and line["e2e_c4"]["offload_jobs"] == 1261
 
 
 def test_bench_two_rank_rehearsal():
@@ -39,6 +42,7 @@ def test_bench_two_rank_rehearsal():
     assert r.returncode == 0, r.stderr[-3000:]
     line = _last_json(r.stdout)
     assert line["n_gpus"] == 2 and line["value"] > 0 and "kv-head shard x2" in line["config"]["parallelism"]
+    assert line["cpu_baseline"]["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
 
 
 def test_reference_arm_line():
