@@ -120,6 +120,12 @@ public:
     Bytes node_bytes(const CacheNode& n) const { return n.token_count() * bpt_; }
     Engine* engine() const { return engine_; }
     void attach_engine(Engine* e);
+    // Prefill emulation (harness / lockstep driver): with no model producing KV, every new
+    // segment gets the deterministic synthetic payload in its fresh HBM slots.
+    // Off by default: in serving, insert only allocates the slots and the model writes the
+    // segment's K/V through kvf_kv_append (include/kvflow.h).
+    void set_prefill_emulation(bool on) { emulate_prefill_ = on; }
+    bool prefill_emulation() const { return emulate_prefill_; }
 
     MatchResult match_prefix(const TokenSeq& tokens, VirtualTime now);
     MatchResult peek_prefix(const TokenSeq& tokens) const;
@@ -172,6 +178,7 @@ private:
 
     Bytes bpt_;
     Engine* engine_ = nullptr;
+    bool emulate_prefill_ = false;
     std::unique_ptr<CacheNode> root_;
     uint64_t next_id_ = 1;
     uint64_t touch_counter_ = 0;

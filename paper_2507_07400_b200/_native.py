@@ -1,8 +1,9 @@
 """ctypes bindings to the in-tree native libraries.
 
   libkvflow.so       -- the CUDA engine C-ABI (include/kvflow.h)
-  libkvflow_host.so  -- the C++ control plane (include/kvflow/*.hpp) behind a small C-ABI
-                        (include/kvflow_host.h) used by tests, smoke() and bench.py
+  libkvflow_host.so  -- the C++ control plane (include/kvflow/*.hpp)
+  libkvflow_driver.so-- harness over it: the synthetic workload generator and the lockstep
+                        driver's C-ABI (include/kvflow_host.h) used by tests, smoke(), bench.py
 
 There is no fallback: if a library is missing this raises, and every engine entry point
 returns KVF_E_NO_DEVICE when no CUDA device is present.
@@ -15,6 +16,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 ENGINE_SO = os.path.join(PKG, "libkvflow.so")
 HOST_SO = os.path.join(PKG, "libkvflow_host.so")
+DRIVER_SO = os.path.join(PKG, "libkvflow_driver.so")
 
 KVF_OK = 0
 KVF_TIER_DEVICE, KVF_TIER_HOST = 0, 1
@@ -141,13 +143,16 @@ def engine_lib():
 
 
 def host_lib():
-    """Load libkvflow_host.so (the C++ control plane).  Raises if it was not built."""
+    """Load the lockstep driver's C-ABI (libkvflow_driver.so over libkvflow_host.so, the C++
+    control plane).  Raises if they were not built."""
     global _host
     if _host is None:
-        engine_lib()  # dependency, loaded first so the loader resolves it in-tree
-        if not os.path.exists(HOST_SO):
-            raise ImportError(f"{HOST_SO} missing: run __graft_entry__.build()")
-        _host = C.CDLL(HOST_SO)
+        engine_lib()  # dependencies, loaded first so the loader resolves them in-tree
+        for so in (HOST_SO, DRIVER_SO):
+            if not os.path.exists(so):
+                raise ImportError(f"{so} missing: run __graft_entry__.build()")
+        C.CDLL(HOST_SO, mode=C.RTLD_GLOBAL)
+        _host = C.CDLL(DRIVER_SO)
         from . import _host_sigs
         _host_sigs.bind(_host)
     return _host

@@ -53,7 +53,9 @@ struct Rig {
     EventQueue ev;
     TierManager tier;
     RadixCache cache;
-    explicit Rig(Bytes cpu_cap = 0) : tier(1 << 20, cpu_cap, flat_cost(), ev, &engine()), cache(kBpt, &engine()) {}
+    explicit Rig(Bytes cpu_cap = 0) : tier(1 << 20, cpu_cap, flat_cost(), ev, &engine()), cache(kBpt, &engine()) {
+        cache.set_prefill_emulation(true);  // the payload checks below need the synthetic KV
+    }
     InsertResult put(const TokenSeq& s, VirtualTime now) {
         InsertResult ins = cache.insert(s, now);
         tier.reserve_working(ins.new_bytes);

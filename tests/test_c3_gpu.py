@@ -24,7 +24,7 @@ def _build():
     exe = os.path.join(ROOT, "tests", "cpp", "c3_kvf")
     src = os.path.join(ROOT, "tests", "cpp", "c3_kvf.cpp")
     subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", f"-I{ROOT}/tests/cpp", src, "-o", exe,
-                    f"-L{PKG}", "-lkvflow_host", "-lkvflow", f"-Wl,-rpath,{PKG}"], check=True)
+                    f"-L{PKG}", "-lkvflow_driver", "-lkvflow_host", "-lkvflow", f"-Wl,-rpath,{PKG}"], check=True)
     return exe
 
 

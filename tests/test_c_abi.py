@@ -18,7 +18,7 @@ def build(tmp_path):
     exe = str(tmp_path / "abi_check")
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.join(ROOT, "include"),
                         os.path.join(ROOT, "tests", "c", "abi_check.c"), "-o", exe, "-L", LIBDIR, "-lkvflow",
-                        "-lkvflow_host", f"-Wl,-rpath,{LIBDIR}"], capture_output=True, text=True, timeout=120)
+                        "-lkvflow_driver", "-lkvflow_host", f"-Wl,-rpath,{LIBDIR}"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     return exe
 

@@ -22,7 +22,7 @@ def build(name):
     if not os.path.exists(exe) or os.path.getmtime(exe) < max(os.path.getmtime(src),
                                                                os.path.getmtime(os.path.join(PKG, "libkvflow_host.so"))):
         subprocess.run(["g++", "-std=c++20", "-O1", "-g", "-Wall", "-Wextra", "-Wno-unused-parameter",
-                        f"-I{ROOT}/include", f"-I{ROOT}/tests/cpp", src, "-o", exe, f"-L{PKG}", "-lkvflow_host",
+                        f"-I{ROOT}/include", f"-I{ROOT}/tests/cpp", src, "-o", exe, f"-L{PKG}", "-lkvflow_driver", "-lkvflow_host",
                         "-lkvflow", f"-Wl,-rpath,{PKG}"], check=True)
     return exe
 
