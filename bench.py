@@ -372,7 +372,13 @@ def run_ours(args, rank, world, local):
                                  "k5_calls": res["evict_calls"], "k5_total": round(res["evict_us"] / 1e3, 2),
                                  "fence_wait": round(res["fence_wait_us"] / 1e3, 2),
                                  "h2d_device": round((res["prefetch_device_ms"] + res["reactive_device_ms"]), 2),
-                                 "d2h_device": round(res["offload_device_ms"], 2)}},
+                                 "d2h_device": round(res["offload_device_ms"], 2),
+                                 "k4_join": round(res["k4_join_us"] / 1e3, 3),
+                                 "k5_calls_only": round(res["k5_us"] / 1e3, 3),
+                                 "victim_apply_incl_k2_issue": round(res["apply_us"] / 1e3, 3),
+                                 "k1_k2_issue": round(res["issue_us"] / 1e3, 3)},
+                "decider": {"resident_served": res["resident_served"], "oneshot_served": res["oneshot_served"],
+                            "resident_launches": res["resident_launches"], "mirror_records": res["mirror_records"]}},
         "latency": {"decision_us_per_agent_step": round(res["decision_us_total"] / steps_e2e, 2),
                     "decision_us_max": round(res["decision_us_max"], 2),
                     "k4_us_per_call": round(res["priority_us"] / max(1, res["priority_calls"]), 2),

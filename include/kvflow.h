@@ -225,6 +225,64 @@ int kvf_priority_propagate(kvf_engine* e, const int32_t* parent, uint32_t n, con
 int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_request* req, int32_t* out_idx,
                       uint8_t* out_action, uint32_t* out_count, uint64_t* out_immediate, uint64_t* out_pending);
 
+/* ---- decisions over a tree mirrored in HBM --------------------------------------------- */
+/* The calls above take a whole SoA snapshot per call.  A kvf_tree keeps the radix tree's SoA
+ * resident in HBM instead, indexed by a stable per-node slot the host assigns (slot 0 = root;
+ * freed slots are reused), and the host sends only the nodes that changed since the last
+ * decision (insert / split / touch / lock / status / backup / removal).  Replaces the
+ * pack-per-call of RadixCache::set_agent_priorities / evict
+ * (proj/src/radix_cache.cpp:266-285, :302-372 walk the live tree on every call).
+ *
+ * Decisions are requests in a ring in mapped pinned memory, executed in order either by a
+ * RESIDENT decider (one 128-thread CTA polling the ring: no launch per decision; trees up to
+ * KVF_RESIDENT_MAX_SLOTS slots) or by one launch per request (larger trees, or the resident
+ * decider disabled).  The resident CTA exits after KVF_DECIDER_IDLE_US (default 200) of idle,
+ * so a device-wide synchronize elsewhere waits at most that long; kvf_decider_hold(e, 1) keeps
+ * it alive across idle gaps (a driver's run), kvf_decider_hold(e, 0) lets it go at once. */
+typedef struct kvf_tree kvf_tree;
+
+#define KVF_SLOT_DEAD 0xFF        /* status of a freed slot */
+#define KVF_RESIDENT_MAX_SLOTS 512u
+
+typedef struct {
+    uint32_t slot;    /* mirror slot of this node */
+    int32_t parent;   /* parent's slot; -1 for the root and for a dead slot */
+    int32_t lock;     /* lock_count (radix_cache.hpp:57) */
+    uint8_t status;   /* NodeStatus 0..3, or KVF_SLOT_DEAD */
+    uint8_t backed;   /* cpu_backed */
+    uint16_t pad0;
+    int64_t rank;     /* host-authored ranks (new nodes SUFFIX, split halves); K4 rewrites them */
+    double time;      /* LastAccess.time */
+    uint64_t seq;     /* LastAccess.seq */
+    uint64_t id;
+    uint64_t tokens;  /* key length */
+    uint64_t pad1;
+} kvf_node_rec;       /* 64 bytes */
+
+int kvf_tree_create(kvf_engine* e, uint64_t bytes_per_token, uint32_t capacity_hint, kvf_tree** out);
+int kvf_tree_destroy(kvf_tree* t);
+/* Stage node records; they reach the mirror ahead of the tree's next decision (last record
+ * of a slot wins).  Slots must be < 2^24. */
+int kvf_tree_update(kvf_tree* t, const kvf_node_rec* recs, uint32_t n);
+/* KVF_TREE_TIME_FOLLOWS_SEQ: every access stamp (time, seq) was taken with a non-decreasing
+ * time and an increasing seq (a cache whose clock never runs backwards) -- then `before`
+ * orders like (seq, id) and the device-wide K5 drops the 8 radix passes over the time word. */
+#define KVF_TREE_TIME_FOLLOWS_SEQ 1u
+int kvf_tree_set_hints(kvf_tree* t, uint32_t hints);
+/* K4 over the mirror (set_agent_priorities): boundary_slot[b] / cand_rank[b] as for
+ * kvf_priority_propagate.  Asynchronous: returns once the request is queued; the mirror's
+ * ranks are updated before any later decision on this tree.  kvf_tree_rank_changes waits for
+ * it and returns the slots whose rank changed (at most the tree's slot count entries). */
+int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m);
+int kvf_tree_rank_changes(kvf_tree* t, uint32_t* slots, int64_t* ranks, uint32_t cap, uint32_t* n_changed);
+/* K5 over the mirror (evict's victim order and actions); victims as slots.  Synchronous. */
+int kvf_tree_victims(kvf_tree* t, const kvf_evict_request* req, uint32_t* out_slot, uint8_t* out_action,
+                     uint32_t cap, uint32_t* out_count, uint64_t* out_immediate, uint64_t* out_pending);
+/* Resident decider control (see above).  hold = 1: never idle out; 0: exit now if idle. */
+int kvf_decider_hold(kvf_engine* e, int32_t hold);
+/* 1 in *running while the resident decider CTA is alive. */
+int kvf_decider_running(kvf_engine* e, int32_t* running);
+
 /* ---- decode-side consumer of the slot-run table ------------------------ */
 /* KV write side of the same layout: store freshly computed K and V of `ntok` tokens for one
  * layer (a prefill chunk, or one decode token per sequence) into HBM slot runs.
@@ -289,6 +347,10 @@ typedef struct {
     double k5_phase_cycles[5]; /* the same phases in SM cycles (clock64)                       */
     uint64_t stale_errors;     /* non-sticky CUDA errors found pending at API entry (cleared) */
     uint64_t attend_calls, attend_bytes; /* K6 calls, KV bytes they read */
+    uint64_t resident_served;  /* mirror decisions served by the resident decider CTA */
+    uint64_t oneshot_served;   /* mirror decisions served by a launch of their own */
+    uint64_t resident_launches;/* resident decider (re)launches */
+    uint64_t mirror_records;   /* node records shipped to tree mirrors */
 } kvf_stats;
 int kvf_get_stats(const kvf_engine* e, kvf_stats* out);
 

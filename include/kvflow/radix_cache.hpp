@@ -7,12 +7,15 @@
 //     splits at any token offset split the run lists (no bytes move);
 //   * insert() gives new nodes HBM slots and writes their payload (prefill emulation);
 //   * set_agent_priorities() runs on the GPU (K4) and evict() takes its victim order from
-//     the GPU (K5) -- the tree is packed as a preorder SoA and shipped per call.
+//     the GPU (K5) over a mirror of the tree kept in HBM (kvf_tree, include/kvflow.h): each
+//     node owns a mirror slot, every mutation marks it, and a decision ships only the
+//     records of the nodes that changed since the previous one.
 // Without an attached Engine the tree still works as a host structure, but priorities and
 // eviction throw ErrorCode::NoDevice (there is no CPU decision path).
 #pragma once
 
 #include <cstdint>
+#include <limits>
 #include <map>
 #include <memory>
 #include <optional>
@@ -28,6 +31,7 @@
 namespace kvf {
 
 class TierManager;
+class RadixCache;
 
 enum class NodeStatus : uint8_t { InGpu = 0, BackupInCpu = 1, Loading = 2, Offloading = 3 };
 const char* status_name(NodeStatus s);
@@ -65,6 +69,11 @@ struct CacheNode {
     RunList host_runs;      // pinned host token slots (cpu_backed, or Offloading destination)
     uint64_t prefix_cid = 0;  // content id of the token before key[0] (payload identity)
     uint64_t end_cid = 0;     // content id of key.back()
+
+    // ---- HBM mirror bookkeeping (RadixCache) ----
+    RadixCache* owner = nullptr;  // the cache whose mirror holds this node
+    uint32_t slot = 0;            // its mirror slot (root: 0)
+    bool mirror_dirty = false;    // changed since the mirror last heard of it
 
     size_t token_count() const { return key.size(); }
     bool is_root() const { return parent == nullptr; }
@@ -137,6 +146,13 @@ public:
 
     // K4 on the GPU: every node SUFFIX, then min(rank_for_step) along boundary root paths.
     void set_agent_priorities(const StepMap& steps);
+    // The same, queued: returns once the request is on the decision ring.  The nodes' ranks
+    // are updated by join_priorities(), which insert / mark_fixed_boundary / evict call first
+    // (a split copies the rank, an evict applies victims); until then node.rank is the old one.
+    void set_agent_priorities_async(const StepMap& steps);
+    void join_priorities();
+    // A node's mirrored fields changed outside the cache (TierManager: status, cpu_backed).
+    void note_changed(CacheNode& n);
     // K5 on the GPU picks the ordered victims; the host applies each action through `tier`.
     EvictOutcome evict(const EvictRequest& req, TierManager& tier, VirtualTime now);
 
@@ -158,10 +174,14 @@ public:
 
     // Content ids of every token of n (walks the prefix chain of its key).
     std::vector<uint64_t> node_cids(const CacheNode& n) const;
-    // Decision-call statistics (wall time of K4/K5 round trips, host pack time).
+    // Decision-call statistics (host wall time of K4/K5 calls; pack = building the change
+    // records; records = node records shipped to the mirror).
     struct DecisionStats {
-        uint64_t priority_calls = 0, evict_calls = 0;
+        uint64_t priority_calls = 0, evict_calls = 0, records = 0;
         double priority_us = 0, evict_us = 0, pack_us = 0;
+        double k4_join_us = 0;  // waiting for queued K4 results (its post is priority_us - this)
+        double k5_us = 0;       // inside kvf_tree_victims (post + wait + copy-out)
+        double apply_us = 0;    // applying the victims' actions (ledger, tier calls, K2 issue)
     };
     const DecisionStats& decision_stats() const { return dstats_; }
 
@@ -173,8 +193,14 @@ private:
     void remove_node(CacheNode* node);
     void drop_boundary_markers(CacheNode* node);
     void require_engine(const char* what) const;
-    // preorder SoA snapshot for K4/K5
-    void pack(bool full);
+    // mirror slots and change records
+    void adopt(CacheNode* n);        // new node: a slot, marked changed
+    void release_slot(CacheNode* n);  // removed node: its slot dead (reused after the next decision)
+    void mark(CacheNode& n);
+    void stamp(CacheNode& n, VirtualTime now);
+    kvf_tree* tree();                 // created on first use (the engine may be attached late)
+    void flush_records();
+    void post_priorities(const StepMap& steps);
 
     Bytes bpt_;
     Engine* engine_ = nullptr;
@@ -184,16 +210,21 @@ private:
     uint64_t touch_counter_ = 0;
     std::unordered_map<AgentId, CacheNode*, AgentIdHash> boundaries_;
 
-    struct Soa {
-        std::vector<CacheNode*> node;
-        std::vector<int32_t> parent, lock;
-        std::vector<uint16_t> depth;
-        std::vector<uint8_t> status, backed;
-        std::vector<int64_t> rank;
-        std::vector<double> time;
-        std::vector<uint64_t> seq, id, tokens;
-        std::unordered_map<const CacheNode*, int32_t> index;
-    } soa_;
+    // the HBM mirror
+    kvf_tree* tree_ = nullptr;
+    Engine* tree_engine_ = nullptr;
+    std::vector<CacheNode*> slot_node_;   // slot -> node (nullptr: dead)
+    std::vector<uint32_t> free_slots_;     // min-heap: slots stay dense
+    std::vector<uint32_t> freed_pending_;  // freed since the last decision: reusable after it
+    std::vector<uint32_t> dirty_;          // slots to ship with the next decision
+    std::vector<kvf_node_rec> recs_;
+    std::vector<uint32_t> chg_slot_, vic_slot_;
+    std::vector<int64_t> chg_rank_;
+    std::vector<uint8_t> vic_act_;
+    bool k4_pending_ = false;
+    bool time_follows_seq_ = true;          // every stamp so far had a non-decreasing time
+    uint32_t hints_sent_ = ~0u;
+    VirtualTime last_stamp_ = -std::numeric_limits<double>::infinity();
     DecisionStats dstats_;
 };
 

@@ -81,6 +81,11 @@ typedef struct {
        C-ABI call time, K4 + K5 together -- the rest of priority_us / evict_us is host packing */
     uint64_t engine_decisions;
     double engine_decision_kernel_ms, engine_decision_call_us;
+    /* HBM tree mirror (kvf_tree): who served the decisions, records shipped */
+    uint64_t resident_served, oneshot_served, resident_launches, mirror_records;
+    /* host-time breakdown (us): waiting for queued K4 results, K5 calls, applying victims
+       (ledger + K2 issue), issuing K1/K2 on the engine */
+    double k4_join_us, k5_us, apply_us, issue_us;
 } kvfh_sim_result;
 
 const char* kvfh_last_error(void);

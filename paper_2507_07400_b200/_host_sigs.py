@@ -35,6 +35,9 @@ class SimResult(C.Structure):
         ("stalled_requests", C.c_uint64), ("measured_requests", C.c_uint64),
         ("engine_decisions", C.c_uint64), ("engine_decision_kernel_ms", C.c_double),
         ("engine_decision_call_us", C.c_double),
+        ("resident_served", C.c_uint64), ("oneshot_served", C.c_uint64), ("resident_launches", C.c_uint64),
+        ("mirror_records", C.c_uint64), ("k4_join_us", C.c_double), ("k5_us", C.c_double), ("apply_us", C.c_double),
+        ("issue_us", C.c_double),
     ]
 
 

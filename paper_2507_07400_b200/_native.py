@@ -65,7 +65,14 @@ class Stats(C.Structure):
                 ("dev_jobs", C.c_uint64), ("decisions", C.c_uint64), ("decision_kernel_ms", C.c_double),
                 ("decision_call_us", C.c_double), ("k5_phase_ns", C.c_double * 5),
                 ("k5_phase_cycles", C.c_double * 5), ("stale_errors", C.c_uint64), ("attend_calls", C.c_uint64),
-                ("attend_bytes", C.c_uint64)]
+                ("attend_bytes", C.c_uint64), ("resident_served", C.c_uint64), ("oneshot_served", C.c_uint64),
+                ("resident_launches", C.c_uint64), ("mirror_records", C.c_uint64)]
+
+
+class NodeRec(C.Structure):  # kvf_node_rec
+    _fields_ = [("slot", C.c_uint32), ("parent", C.c_int32), ("lock", C.c_int32), ("status", C.c_uint8),
+                ("backed", C.c_uint8), ("pad0", C.c_uint16), ("rank", C.c_int64), ("time", C.c_double),
+                ("seq", C.c_uint64), ("id", C.c_uint64), ("tokens", C.c_uint64), ("pad1", C.c_uint64)]
 
 
 # every symbol include/kvflow.h declares, with its ctypes signature
@@ -121,6 +128,17 @@ _ENGINE_SIGS = {
     "kvf_payload_checksum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "kvf_read_runs": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_get_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "kvf_tree_create": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "kvf_tree_destroy": (C.c_int, [C.c_void_p]),
+    "kvf_tree_set_hints": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "kvf_tree_update": (C.c_int, [C.c_void_p, C.POINTER(NodeRec), C.c_uint32]),
+    "kvf_tree_priorities": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.c_uint32]),
+    "kvf_tree_rank_changes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.c_uint32,
+                                        C.POINTER(C.c_uint32)]),
+    "kvf_tree_victims": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), C.c_uint32,
+                                   C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "kvf_decider_hold": (C.c_int, [C.c_void_p, C.c_int32]),
+    "kvf_decider_running": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
 }
 
 _engine = None

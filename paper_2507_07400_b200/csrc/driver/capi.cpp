@@ -282,6 +282,14 @@ int kvfh_sim_result_get(const kvfh_sim* s, kvfh_sim_result* r) {
         r->engine_decisions = es.decisions;
         r->engine_decision_kernel_ms = es.decision_kernel_ms;
         r->engine_decision_call_us = es.decision_call_us;
+        r->resident_served = es.resident_served;
+        r->oneshot_served = es.oneshot_served;
+        r->resident_launches = es.resident_launches;
+        r->mirror_records = es.mirror_records;
+        r->k4_join_us = d.k4_join_us;
+        r->k5_us = d.k5_us;
+        r->apply_us = d.apply_us;
+        r->issue_us = s->sim->tier().issue_us();
         r->verified_loads = s->sim->verified_loads;
         r->verify_failures = s->sim->verify_failures;
         r->audits = s->audits;

@@ -1,18 +1,22 @@
-// K5, device-wide path for trees above the single-CTA limit (4096 nodes).
+// K5, device-wide path for trees above the single-CTA limit (4096 slots).  Hand-written
+// grid kernels, no library sort.
 //
-// Same closed form as the single-CTA kernel (decide.cu), spread over the
-// whole GPU:
-//   1. stage flags (self-eligible, releases-parent) per node            -- 1 grid kernel
-//   2. `before` order of the candidates as a stable LSD radix sort       -- CUB onesweep, one
-//      pass per key word, least significant first: id, seq, time, (rank)  pass per word
-//      and finally a 1-bit "not a candidate" word so non-candidates sort last
-//   3. ord, blocked root walks, R, eff root walks                         -- 4 grid kernels
-//      (global atomics with early exit, as in the CTA version)
-//   4. victims: R sorted by (eff asc, depth desc)                         -- CUB radix sort
-//   5. byte prefix in victim order + the `needed` cut + actions           -- CUB scan + 1 kernel
-// No host round trip between phases; one H2D of the packed SoA and one D2H of the result.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
+// Same closed form as the single-CTA kernel (decide_body.cuh), reorganised so
+// only ONE sort is needed:
+//   1. flags per node (self-eligible, releases-parent); candidates compacted      -- 1 kernel
+//   2. blocked root walks -> R                                                    -- 1 kernel
+//   3. `before` order of the candidates (radix_cache.cpp:316-321) by a stable LSD radix
+//      sort, 8-bit digits, least significant word first: id, seq, [time], [rank desc] --
+//      each word only over the bytes its largest value uses; time is skipped when access
+//      times follow access sequence numbers (the cache says so)                    -- 3 kernels/digit
+//   4. ord[x] = sorted position; eff(n) = max ord over n's R-subtree by root walks -- 2 kernels
+//   5. victims WITHOUT a second sort: R sorted by (eff asc, depth desc) is a sequence of
+//      chains -- each R node y with eff(y) = ord(y) heads the chain y, parent(y), ... of the
+//      ancestors whose eff is ord(y), deepest first -- and the chain heads come in sorted
+//      position order.  So: chain bytes per sorted position, an exclusive scan, and every chain
+//      member whose bytes-before is < needed is a victim (radix_cache.cpp:335)      -- 3 kernels
+// Everything is captured once per (padded size, key widths, policy) as a CUDA graph; the
+// request lives in device memory, so a call = request upload + graph launch + one sync.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,28 +30,20 @@ namespace {
 
 constexpr int64_t kSuffix = INT64_MAX / 2;
 constexpr int64_t kUnreach = INT64_MAX / 4;
+constexpr uint32_t kTile = 2048;  // radix tile: 256 threads x 8 elements
+constexpr uint32_t kThr = 256;
 
-struct BigTree {
-    const int32_t* parent;
-    const uint16_t* depth;
-    const uint8_t* status;
-    const int32_t* lock;
-    const int64_t* rank;
-    const double* time;
-    const uint64_t* seq;
-    const uint64_t* id;
-    const uint64_t* tokens;
-    const uint8_t* backed;
-    uint32_t n;
-};
-
-struct BigReq {  // lives in device memory (part of the uploaded blob): the graph is reusable
+struct BigReq {  // device memory, uploaded per call
     uint64_t needed;
     int64_t floor;
     uint64_t cpu_used, cpu_cap;
-    int32_t wa, offload, has_floor;
-    uint64_t bpt;  // bytes per token (per call: not baked into the graph)
-    int64_t rank_max;  // rank_bytes < 8: every rank is SUFFIX, UNREACHABLE or in [0, rank_max]
+    int32_t wa, offload, has_floor, pad;
+    uint64_t bpt;
+    int64_t rank_max;  // compact WA rank code: SUFFIX -> 0, UNREACHABLE -> 1, r -> 2 + rank_max - r
+};
+
+struct Hdr {  // device memory, zeroed per call
+    unsigned long long count, imm, pend, cands;
 };
 
 __device__ __forceinline__ uint64_t time_order(double t) {
@@ -55,78 +51,166 @@ __device__ __forceinline__ uint64_t time_order(double t) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void big_stage(BigTree t, const BigReq* __restrict__ q, uint8_t* flags, uint32_t* blocked, uint32_t* vals) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
-        const uint64_t bytes = t.tokens[i] * q->bpt;
+// 1. flags (bit0 selfok, bit1 releases), blocked = 0, ord = -1; candidates -> vals (any order:
+//    the sort key is total, ids are unique)
+__global__ void __launch_bounds__(kThr) big_stage(LargeArrays a, uint32_t np, const BigReq* __restrict__ q,
+                                                  uint8_t* flags, uint32_t* blocked, int32_t* ord, uint32_t* vals,
+                                                  Hdr* hdr) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+        const uint64_t bytes = a.tokens[i] * q->bpt;
         const bool cpu_room = q->cpu_cap == 0 || q->cpu_used + bytes <= q->cpu_cap;
-        const bool selfok =
-            i > 0 && t.lock[i] == 0 && t.status[i] == 0 && (!q->has_floor || t.rank[i] > q->floor);
-        const bool releases = !q->offload || t.backed[i] || !cpu_room;
+        const bool selfok = i > 0 && a.status[i] == 0 && a.lock[i] == 0 && (!q->has_floor || a.rank[i] > q->floor);
+        const bool releases = !q->offload || a.backed[i] || !cpu_room;
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
         blocked[i] = 0;
-        vals[i] = i;
+        ord[i] = -1;
+        // warp-aggregated slot in the candidate list
+        const unsigned act = __activemask();
+        const unsigned mask = __ballot_sync(act, selfok);
+        const int leader = __ffs(act) - 1;
+        const int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == leader && mask) base = atomicAdd(&hdr->cands, static_cast<unsigned long long>(__popc(mask)));
+        base = __shfl_sync(act, base, leader);
+        if (selfok) vals[base + __popc(mask & ((1u << lane) - 1u))] = i;
     }
 }
 
-// keys[k] = word `w` of node vals[k]'s `before` key (ascending = earlier).  Only the relative
-// order of candidates matters downstream (ord is read for R nodes only), so non-candidates
-// need no extra pass to sort last.
-// WA rank word, descending.  Compact form (rank_bytes < 8, decided on the host): SUFFIX -> 0,
-// UNREACHABLE -> 1, r in [0, rank_max] -> 2 + rank_max - r -- the same order in a few bytes.
-__device__ __forceinline__ uint64_t rank_key(int64_t r, const BigReq* q, bool compact) {
-    if (!compact) return ~(static_cast<uint64_t>(r) ^ 0x8000000000000000ull);
-    if (r == kSuffix) return 0;
-    if (r == kUnreach) return 1;
-    return 2 + static_cast<uint64_t>(q->rank_max - r);
-}
-
-__global__ void big_gather_key(BigTree t, const BigReq* q, const uint32_t* vals, uint64_t* keys, int w,
-                               bool compact_rank) {
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
-        const uint32_t i = vals[k];
-        uint64_t key;
-        switch (w) {
-            case 0: key = t.id[i]; break;
-            case 1: key = t.seq[i]; break;
-            case 2: key = time_order(t.time[i]); break;
-            default: key = rank_key(t.rank[i], q, compact_rank); break;  // rank desc
-        }
-        keys[k] = key;
-    }
-}
-
-__global__ void big_ord(uint32_t n, const uint32_t* vals, int32_t* ord) {
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) ord[vals[k]] = k;
-}
-
-__global__ void big_blocked(BigTree t, const uint8_t* flags, uint32_t* blocked) {
-    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < t.n; m += gridDim.x * blockDim.x) {
+// 2. blocked(p): some device node below p is not self-eligible or would not release it
+//    (has_device_child, radix_cache.cpp:40-45); walkers stop where another already passed
+__global__ void __launch_bounds__(kThr) big_blocked(LargeArrays a, uint32_t np, const uint8_t* flags, uint32_t* blocked) {
+    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < np; m += gridDim.x * blockDim.x) {
         const uint8_t f = flags[m];
-        if (t.status[m] == 1 || ((f & 1) && (f & 2))) continue;
+        const uint8_t s = a.status[m];
+        if (s == 1 || s == KVF_SLOT_DEAD || ((f & 1) && (f & 2))) continue;
         for (int32_t cur = static_cast<int32_t>(m);;) {
-            const int32_t p = t.parent[cur];
+            const int32_t p = a.parent[cur];
             if (p <= 0) break;
             if (atomicOr(&blocked[p], 1u)) break;
-            if (t.status[p] == 1) break;
+            if (a.status[p] == 1) break;
             cur = p;
         }
     }
 }
 
-__global__ void big_r_init(uint32_t n, uint8_t* flags, const uint32_t* blocked, const int32_t* ord, int32_t* eff) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+// 3. one 8-bit digit of the `before` key; word w: 0 id, 1 seq, 2 time, 3 rank (descending)
+__device__ __forceinline__ uint32_t digit(const LargeArrays& a, const BigReq* q, uint32_t node, int w, int byte,
+                                          bool compact_rank) {
+    uint64_t k;
+    switch (w) {
+        case 0: k = a.id[node]; break;
+        case 1: k = a.seq[node]; break;
+        case 2: k = time_order(a.time[node]); break;
+        default: {
+            const int64_t r = a.rank[node];
+            if (!compact_rank) k = ~(static_cast<uint64_t>(r) ^ 0x8000000000000000ull);
+            else if (r == kSuffix) k = 0;
+            else if (r == kUnreach) k = 1;
+            else k = 2 + static_cast<uint64_t>(q->rank_max - r);
+        }
+    }
+    return static_cast<uint32_t>(k >> (8 * byte)) & 0xFFu;
+}
+
+__global__ void __launch_bounds__(kThr) big_hist(LargeArrays a, const BigReq* q, const uint32_t* vals, const Hdr* hdr,
+                                                 uint32_t* hist, int w, int byte, bool compact) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t c = static_cast<uint32_t>(hdr->cands);
+    const uint32_t base = blockIdx.x * kTile;
+    if (base < c) {
+        for (uint32_t k = base + threadIdx.x; k < min(c, base + kTile); k += kThr)
+            atomicAdd(&h[digit(a, q, vals[k], w, byte, compact)], 1u);
+    }
+    __syncthreads();
+    hist[blockIdx.x * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+// offsets[t][d] = (elements with digit < d) + (digit-d elements of tiles < t); in place
+__global__ void __launch_bounds__(kThr) big_offsets(uint32_t* hist, uint32_t tiles) {
+    __shared__ uint32_t tot[256];
+    const uint32_t d = threadIdx.x;
+    uint32_t run = 0;
+    for (uint32_t t = 0; t < tiles; ++t) {
+        const uint32_t v = hist[t * 256 + d];
+        hist[t * 256 + d] = run;
+        run += v;
+    }
+    tot[d] = run;
+    __syncthreads();
+    for (uint32_t off = 1; off < 256; off <<= 1) {  // inclusive scan over digits
+        const uint32_t y = d >= off ? tot[d - off] : 0;
+        __syncthreads();
+        tot[d] += y;
+        __syncthreads();
+    }
+    const uint32_t base = tot[d] - run;
+    for (uint32_t t = 0; t < tiles; ++t) hist[t * 256 + d] += base;
+}
+
+// stable scatter: a tile in 8 rounds of 256 elements in index order; within a round, equal
+// digits are ranked by warp (match) and lane
+__global__ void __launch_bounds__(kThr) big_scatter(LargeArrays a, const BigReq* q, const uint32_t* vin, uint32_t* vout,
+                                                    const Hdr* hdr, const uint32_t* offsets, int w, int byte,
+                                                    bool compact) {
+    __shared__ uint32_t run[256];
+    __shared__ uint16_t cnt[kThr / 32][256];
+    const uint32_t c = static_cast<uint32_t>(hdr->cands);
+    const uint32_t base = blockIdx.x * kTile;
+    if (base >= c) return;  // uniform per CTA
+    run[threadIdx.x] = offsets[blockIdx.x * 256 + threadIdx.x];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t r = 0; r < kTile / kThr; ++r) {
+        for (uint32_t w8 = 0; w8 < kThr / 32; ++w8) cnt[w8][threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t k = base + r * kThr + threadIdx.x;
+        const bool live = k < c;
+        uint32_t v = 0, d = 256;
+        if (live) {
+            v = vin[k];
+            d = digit(a, q, v, w, byte, compact);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rk = __popc(peers & ((1u << lane) - 1u));
+        if (live && rk == 0) cnt[warp][d] = static_cast<uint16_t>(__popc(peers));
+        __syncthreads();
+        if (live) {
+            uint32_t pre = 0;
+            for (uint32_t w8 = 0; w8 < warp; ++w8) pre += cnt[w8][d];
+            vout[run[d] + pre + rk] = v;
+        }
+        __syncthreads();
+        uint32_t add = 0;
+        for (uint32_t w8 = 0; w8 < kThr / 32; ++w8) add += cnt[w8][threadIdx.x];
+        run[threadIdx.x] += add;
+        __syncthreads();
+    }
+}
+
+// 4. ord, R, eff
+__global__ void __launch_bounds__(kThr) big_ord(const uint32_t* vals, const Hdr* hdr, int32_t* ord) {
+    const uint32_t c = static_cast<uint32_t>(hdr->cands);
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
+        ord[vals[k]] = static_cast<int32_t>(k);
+}
+
+__global__ void __launch_bounds__(kThr) big_r_init(uint32_t np, uint8_t* flags, const uint32_t* blocked,
+                                                   const int32_t* ord, int32_t* eff) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
         const bool r = (flags[i] & 1) && !blocked[i];
         if (r) flags[i] |= 4;
         eff[i] = r ? ord[i] : -1;
     }
 }
 
-__global__ void big_eff(BigTree t, const uint8_t* flags, const int32_t* ord, int32_t* eff) {
-    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < t.n; m += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kThr) big_eff(LargeArrays a, uint32_t np, const uint8_t* flags, const int32_t* ord,
+                                                int32_t* eff) {
+    for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x + 1; m < np; m += gridDim.x * blockDim.x) {
         if (!(flags[m] & 4)) continue;
         const int32_t v = ord[m];
         for (int32_t cur = static_cast<int32_t>(m);;) {
-            const int32_t p = t.parent[cur];
+            const int32_t p = a.parent[cur];
             if (p <= 0 || !(flags[p] & 4)) break;
             if (atomicMax(&eff[p], v) >= v) break;
             cur = p;
@@ -134,52 +218,141 @@ __global__ void big_eff(BigTree t, const uint8_t* flags, const int32_t* ord, int
     }
 }
 
-// victim key (eff asc, depth desc) in 16 + log2(n) + 1 bits; non-R nodes sort last
-__global__ void big_victim_keys(BigTree t, const uint8_t* flags, const int32_t* eff, uint64_t* keys, uint32_t* vals) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += gridDim.x * blockDim.x) {
-        keys[i] = (flags[i] & 4) ? (static_cast<uint64_t>(static_cast<uint32_t>(eff[i])) << 16) |
-                                       (0xFFFFu - static_cast<uint32_t>(t.depth[i]))
-                                 : ~0ull;
-        vals[i] = i;
+// 5. chains.  Sorted position k heads a chain iff its node y is in R and eff(y) == k.
+__device__ __forceinline__ bool chain_head(const uint32_t* vals, const uint8_t* flags, const int32_t* eff, uint32_t k,
+                                           uint32_t c, uint32_t* y) {
+    if (k >= c) return false;
+    *y = vals[k];
+    return (flags[*y] & 4) && eff[*y] == static_cast<int32_t>(k);
+}
+
+template <typename F>
+__device__ __forceinline__ void walk_chain(const LargeArrays& a, const uint8_t* flags, const int32_t* eff, uint32_t y,
+                                           int32_t k, F f) {
+    for (int32_t cur = static_cast<int32_t>(y);;) {
+        f(static_cast<uint32_t>(cur));
+        const int32_t p = a.parent[cur];
+        if (p <= 0 || !(flags[p] & 4) || eff[p] != k) break;
+        cur = p;
     }
 }
 
-__global__ void big_bytes(BigTree t, const BigReq* __restrict__ q, const uint64_t* keys, const uint32_t* vals,
-                          uint64_t* bytes) {
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x)
-        bytes[k] = keys[k] == ~0ull ? 0 : t.tokens[vals[k]] * q->bpt;
+// Block-wide exclusive scan of (bytes, count) pairs, kTile per block (8 per thread, in order).
+struct Pair {
+    unsigned long long b;
+    uint32_t n;
+};
+__device__ __forceinline__ Pair block_excl(Pair mine, Pair* total) {
+    __shared__ unsigned long long sb[kThr / 32];
+    __shared__ uint32_t sn[kThr / 32];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    Pair inc = mine;
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long yb = __shfl_up_sync(0xffffffffu, inc.b, off);
+        const uint32_t yn = __shfl_up_sync(0xffffffffu, inc.n, off);
+        if (lane >= static_cast<uint32_t>(off)) {
+            inc.b += yb;
+            inc.n += yn;
+        }
+    }
+    if (lane == 31) {
+        sb[warp] = inc.b;
+        sn[warp] = inc.n;
+    }
+    __syncthreads();
+    Pair before{0, 0}, all{0, 0};
+    for (uint32_t w8 = 0; w8 < kThr / 32; ++w8) {
+        if (w8 < warp) {
+            before.b += sb[w8];
+            before.n += sn[w8];
+        }
+        all.b += sb[w8];
+        all.n += sn[w8];
+    }
+    __syncthreads();
+    if (total) *total = all;
+    return Pair{before.b + inc.b - mine.b, before.n + inc.n - mine.n};
 }
 
-// victim k is popped iff the bytes freed before it are < needed (radix_cache.cpp:335);
-// idx / action go straight to mapped pinned host memory (posted writes, no D2H copy)
-__global__ void big_cut(BigTree t, const BigReq* __restrict__ q, const uint64_t* keys, const uint32_t* vals,
-                        const uint64_t* before, int32_t* out_idx, uint8_t* out_act, unsigned long long* header) {
-    uint64_t imm = 0, pend = 0;
-    uint32_t cnt = 0;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < t.n; k += gridDim.x * blockDim.x) {
-        if (keys[k] == ~0ull || before[k] >= q->needed) continue;
-        const uint32_t v = vals[k];
-        const uint64_t bytes = t.tokens[v] * q->bpt;
-        uint8_t act;
-        if (!q->offload) act = KVF_ACT_REMOVE;
-        else if (t.backed[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
-        else if (!(q->cpu_cap == 0 || q->cpu_used + bytes <= q->cpu_cap)) act = KVF_ACT_REMOVE;
-        else act = KVF_ACT_OFFLOAD;
-        out_idx[k] = static_cast<int32_t>(v);
-        out_act[k] = act;
-        (act == KVF_ACT_OFFLOAD ? pend : imm) += bytes;
-        cnt = max(cnt, k + 1);
+__device__ __forceinline__ Pair thread_chunk(const LargeArrays& a, const BigReq* q, const uint32_t* vals,
+                                             const uint8_t* flags, const int32_t* eff, uint32_t c, uint32_t k0,
+                                             Pair* per /* [8] or null */) {
+    Pair s{0, 0};
+    for (uint32_t j = 0; j < kTile / kThr; ++j) {
+        uint32_t y;
+        Pair p{0, 0};
+        if (chain_head(vals, flags, eff, k0 + j, c, &y))
+            walk_chain(a, flags, eff, y, static_cast<int32_t>(k0 + j), [&](uint32_t v) {
+                p.b += a.tokens[v] * q->bpt;
+                p.n += 1;
+            });
+        if (per) per[j] = p;
+        s.b += p.b;
+        s.n += p.n;
     }
-    for (int o = 16; o; o >>= 1) {
-        imm += __shfl_xor_sync(0xffffffffu, imm, o);
-        pend += __shfl_xor_sync(0xffffffffu, pend, o);
-        cnt = max(cnt, __shfl_xor_sync(0xffffffffu, cnt, o));
+    return s;
+}
+
+__global__ void __launch_bounds__(kThr) big_tile_sums(LargeArrays a, const BigReq* q, const uint32_t* vals,
+                                                      const uint8_t* flags, const int32_t* eff, const Hdr* hdr,
+                                                      Pair* tsum) {
+    const uint32_t c = static_cast<uint32_t>(hdr->cands);
+    const uint32_t k0 = blockIdx.x * kTile + threadIdx.x * (kTile / kThr);
+    Pair tot;
+    block_excl(thread_chunk(a, q, vals, flags, eff, c, k0, nullptr), &tot);
+    if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kThr) big_tile_scan(Pair* tsum, uint32_t tiles) {
+    if (threadIdx.x == 0) {  // tiles <= ~100: serial is shorter than a block scan's barriers
+        Pair run{0, 0};
+        for (uint32_t t = 0; t < tiles; ++t) {
+            const Pair v = tsum[t];
+            tsum[t] = run;
+            run.b += v.b;
+            run.n += v.n;
+        }
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (cnt) atomicMax(header, static_cast<unsigned long long>(cnt));
-        if (imm) atomicAdd(header + 1, static_cast<unsigned long long>(imm));
-        if (pend) atomicAdd(header + 2, static_cast<unsigned long long>(pend));
+}
+
+// every chain member whose bytes-before is still < needed is popped (radix_cache.cpp:335);
+// slots and actions go straight to mapped pinned memory
+__global__ void __launch_bounds__(kThr) big_emit(LargeArrays a, const BigReq* q, const uint32_t* vals,
+                                                 const uint8_t* flags, const int32_t* eff, Hdr* hdr, const Pair* tsum,
+                                                 uint32_t* out_idx, uint8_t* out_act) {
+    const uint32_t c = static_cast<uint32_t>(hdr->cands);
+    const uint32_t k0 = blockIdx.x * kTile + threadIdx.x * (kTile / kThr);
+    Pair per[kTile / kThr];
+    const Pair mine = thread_chunk(a, q, vals, flags, eff, c, k0, per);
+    Pair pre = block_excl(mine, nullptr);
+    pre.b += tsum[blockIdx.x].b;
+    pre.n += tsum[blockIdx.x].n;
+    if (pre.b >= q->needed) return;
+    unsigned long long imm = 0, pend = 0, cnt = 0;
+    for (uint32_t j = 0; j < kTile / kThr && pre.b < q->needed; ++j) {
+        uint32_t y;
+        if (per[j].n && chain_head(vals, flags, eff, k0 + j, c, &y)) {
+            walk_chain(a, flags, eff, y, static_cast<int32_t>(k0 + j), [&](uint32_t v) {
+                const uint64_t bytes = a.tokens[v] * q->bpt;
+                if (pre.b < q->needed) {
+                    uint8_t act;
+                    if (!q->offload) act = KVF_ACT_REMOVE;
+                    else if (a.backed[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
+                    else if (!(q->cpu_cap == 0 || q->cpu_used + bytes <= q->cpu_cap)) act = KVF_ACT_REMOVE;
+                    else act = KVF_ACT_OFFLOAD;
+                    out_idx[pre.n] = v;
+                    out_act[pre.n] = act;
+                    (act == KVF_ACT_OFFLOAD ? pend : imm) += bytes;
+                    cnt = max(cnt, static_cast<unsigned long long>(pre.n) + 1);
+                }
+                pre.b += bytes;
+                pre.n += 1;
+            });
+        }
     }
+    if (cnt) atomicMax(&hdr->count, cnt);
+    if (imm) atomicAdd(&hdr->imm, imm);
+    if (pend) atomicAdd(&hdr->pend, pend);
 }
 
 template <typename T>
@@ -189,18 +362,9 @@ T* take(char*& p, size_t count) {
     return r;
 }
 
-// Bucketed size: n rounded up to a quarter of its octave (<= 25 % padding), so a captured
-// graph serves every tree size in the bucket.
-uint32_t bucket(uint32_t n) {
-    uint32_t p = 1;
-    while (p * 2 <= n) p *= 2;
-    const uint32_t step = std::max<uint32_t>(1024, p / 4);
-    return (n + step - 1) / step * step;
-}
-
-uint32_t bits_for(uint32_t x) {  // bits to hold 0..x
-    uint32_t b = 0;
-    while ((1ull << b) <= x) ++b;
+uint32_t live_bytes(uint64_t x) {
+    uint32_t b = 1;
+    while (b < 8 && (x >> (8 * b))) ++b;
     return b;
 }
 
@@ -208,152 +372,102 @@ uint32_t bits_for(uint32_t x) {  // bits to hold 0..x
 
 namespace kvf_impl {
 
-int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
-                        uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend) {
-    const uint32_t n = t->n;
-    const uint32_t np = bucket(n);
+// Padded size: n rounded up to a quarter of its octave (<= 25 % padding), so one captured
+// graph serves every tree size in the bucket; a multiple of the radix tile.
+uint32_t large_capacity(uint32_t n) {
+    uint32_t p = 1;
+    while (p * 2 <= n) p *= 2;
+    const uint32_t step = std::max<uint32_t>(kTile, p / 4);
+    return (n + step - 1) / step * step;
+}
+
+void large_invalidate(LargeState& st) {
+    for (auto& kv : st.graphs) cudaGraphExecDestroy(kv.second.exec);
+    st.graphs.clear();
+    st.baked = nullptr;
+}
+
+void large_release(LargeState& st) {
+    large_invalidate(st);
+    st.ws.release();
+}
+
+int victim_large(kvf_engine* e, LargeState& st, const LargeArrays& a, const kvf_evict_request* q, uint64_t bpt,
+                 const LargeKeyInfo& keys, uint32_t* out_idx, uint8_t* out_action, uint32_t cap, uint32_t* out_count,
+                 uint64_t* out_imm, uint64_t* out_pend) {
+    const uint32_t np = large_capacity(a.n);
+    const uint32_t tiles = np / kTile;
     const bool wa = q->workflow_aware != 0;
     cudaStream_t s = e->s_dec;
-    size_t sort_tmp = 0, scan_tmp = 0;
-    KVF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, static_cast<uint64_t*>(nullptr),
-                                             static_cast<uint64_t*>(nullptr), static_cast<uint32_t*>(nullptr),
-                                             static_cast<uint32_t*>(nullptr), static_cast<int>(np), 0, 64, s));
-    KVF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, static_cast<uint64_t*>(nullptr),
-                                           static_cast<uint64_t*>(nullptr), static_cast<int>(np), s));
-    const size_t in_bytes = 256 + static_cast<size_t>(np) * (8 * 5 + 4 * 2 + 2 + 2) + 16 * 256;
-    const size_t out_bytes = 256 + static_cast<size_t>(np) * 5 + 2 * 256;
-    const size_t work_bytes = static_cast<size_t>(np) * (1 + 4 + 4 + 4 + 8 * 2 + 4 * 2 + 8 * 2) + sort_tmp +
-                              scan_tmp + 64 * 256;
-    const void* old_dev = e->ws_big.dev;
-    const void* old_host = e->ws_big.host;
-    int rc = e->ws_big.ensure(in_bytes + work_bytes, in_bytes + out_bytes);
-    if (rc) return rc;
-    if (e->ws_big.dev != old_dev || e->ws_big.host != old_host) {  // graphs bake the old pointers
-        for (auto& kv : e->big_graphs) cudaGraphExecDestroy(kv.second.exec);
-        e->big_graphs.clear();
-    }
-    // ---- pack the SoA (+ padding nodes that are never candidates) and the request ----
-    char* h = static_cast<char*>(e->ws_big.host);
-    char* hp = h;
-    BigReq* hreq = take<BigReq>(hp, 1);
-    *hreq = BigReq{q->needed,       q->floor,        q->cpu_used,  q->cpu_capacity, q->workflow_aware,
-                   q->offload_mode, q->has_floor, t->bytes_per_token};
-    auto put = [&](auto* src, size_t elem, int fill) {
-        char* dst = hp;
-        std::memcpy(dst, src, n * elem);
-        std::memset(dst + n * elem, fill, (np - n) * elem);
-        hp += (np * elem + 255) & ~size_t(255);
-    };
-    put(t->rank, 8, 0);
-    put(t->time, 8, 0);
-    put(t->seq, 8, 0);
-    put(t->id, 8, 0);
-    put(t->tokens, 8, 0);
-    put(t->parent, 4, 0xFF);  // parent -1: walks stop at once
-    put(t->lock, 4, 0);
-    put(t->depth, 2, 0);
-    put(t->status, 1, 2);     // not IN_GPU: never a candidate, never R
-    put(t->backed, 1, 0);
-    const size_t used = static_cast<size_t>(hp - h);
-    char* hout = h + ((used + 255) & ~size_t(255));
-    unsigned long long* hhdr = reinterpret_cast<unsigned long long*>(hout);
-    char* hout_dev = static_cast<char*>(e->ws_big.host_dev) + (hout - h);
-    int32_t* o_idx = reinterpret_cast<int32_t*>(hout_dev + 256);
-    uint8_t* o_act = reinterpret_cast<uint8_t*>(hout_dev + 256 + ((np * 4ull + 255) & ~255ull));
-
-    // node ids and access sequence numbers are counters: their LSD passes only need the bytes
-    // the largest one uses (8 CUB passes per 64-bit word otherwise; padding nodes hold 0)
-    uint64_t max_id = 0, max_seq = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-        max_id = std::max(max_id, t->id[i]);
-        max_seq = std::max(max_seq, t->seq[i]);
-    }
-    auto live_bytes = [](uint64_t x) {
-        uint32_t b = 1;
-        while (b < 8 && (x >> (8 * b))) ++b;
-        return b;
-    };
-    const uint32_t id_bytes = live_bytes(max_id), seq_bytes = live_bytes(max_seq);
-    // WA: ranks are SUFFIX, UNREACHABLE or small step ranks (radix_cache.hpp:30-38) -> a compact
-    // order-preserving code (rank_key); anything else keeps the full 64-bit word
-    uint32_t rank_bytes = 8;
-    if (wa) {
-        int64_t rmax = 0;
-        bool small = true;
-        for (uint32_t i = 0; i < n && small; ++i) {
-            const int64_t r = t->rank[i];
-            if (r == kSuffix || r == kUnreach) continue;
-            if (r < 0 || r > (int64_t{1} << 40)) small = false;
-            else rmax = std::max(rmax, r);
-        }
-        if (small) {
-            rank_bytes = live_bytes(static_cast<uint64_t>(rmax) + 2);
-            hreq->rank_max = rmax;
-        }
-    }
-    const uint64_t key = (static_cast<uint64_t>(np) << 13) | (rank_bytes << 9) | (id_bytes << 5) | (seq_bytes << 1) |
-                         (wa ? 1u : 0u);
-    auto git = e->big_graphs.find(key);
-    if (git == e->big_graphs.end()) {
-        // ---- capture the whole device-wide sequence once per (bucket, policy, key widths) ----
-        char* d = static_cast<char*>(e->ws_big.dev);
+    const size_t work = 256 * 8 + static_cast<size_t>(np) * (1 + 4 + 4 + 4 + 4 + 4) + static_cast<size_t>(tiles) * (256 * 4 + 16) +
+                        16 * 256;
+    const size_t host = 512 + static_cast<size_t>(np) * 5 + 2 * 256;
+    const void* old_dev = st.ws.dev;
+    const void* old_host = st.ws.host;
+    if (int rc = st.ws.ensure(work, host)) return rc;
+    if (st.ws.dev != old_dev || st.ws.host != old_host || st.baked != a.parent) large_invalidate(st);
+    st.baked = a.parent;
+    // key widths (padding slots hold 0s)
+    const uint32_t id_bytes = live_bytes(keys.max_id), seq_bytes = live_bytes(keys.max_seq);
+    const bool compact = keys.rank_small;
+    const uint32_t rank_bytes = compact ? live_bytes(static_cast<uint64_t>(keys.rank_max) + 2) : 8;
+    const bool skip_time = keys.time_follows_seq;
+    const uint64_t key = (static_cast<uint64_t>(np) << 16) | (rank_bytes << 12) | (id_bytes << 8) | (seq_bytes << 4) |
+                         (skip_time ? 2u : 0u) | (wa ? 1u : 0u);
+    char* h = static_cast<char*>(st.ws.host);
+    BigReq* hreq = reinterpret_cast<BigReq*>(h);
+    *hreq = BigReq{q->needed, q->floor, q->cpu_used, q->cpu_capacity, q->workflow_aware, q->offload_mode,
+                   q->has_floor, 0, bpt, keys.rank_max};
+    char* hout = h + 512;
+    uint32_t* h_idx = reinterpret_cast<uint32_t*>(hout);
+    uint8_t* h_act = reinterpret_cast<uint8_t*>(hout + ((np * 4ull + 255) & ~255ull));
+    Hdr* h_hdr = reinterpret_cast<Hdr*>(h + 256);
+    char* hdev = static_cast<char*>(st.ws.host_dev);
+    uint32_t* o_idx = reinterpret_cast<uint32_t*>(hdev + 512);
+    uint8_t* o_act = reinterpret_cast<uint8_t*>(hdev + 512 + ((np * 4ull + 255) & ~255ull));
+    char* d = static_cast<char*>(st.ws.dev);
+    auto git = st.graphs.find(key);
+    if (git == st.graphs.end()) {
         char* dp = d;
-        const BigReq* dreq = take<BigReq>(dp, 1);
-        BigTree bt;
-        bt.rank = take<int64_t>(dp, np);
-        bt.time = take<double>(dp, np);
-        bt.seq = take<uint64_t>(dp, np);
-        bt.id = take<uint64_t>(dp, np);
-        bt.tokens = take<uint64_t>(dp, np);
-        bt.parent = take<int32_t>(dp, np);
-        bt.lock = take<int32_t>(dp, np);
-        bt.depth = take<uint16_t>(dp, np);
-        bt.status = take<uint8_t>(dp, np);
-        bt.backed = take<uint8_t>(dp, np);
-        bt.n = np;
+        BigReq* dreq = take<BigReq>(dp, 1);
+        Hdr* dhdr = take<Hdr>(dp, 1);
         uint8_t* flags = take<uint8_t>(dp, np);
         uint32_t* blocked = take<uint32_t>(dp, np);
         int32_t* ord = take<int32_t>(dp, np);
         int32_t* eff = take<int32_t>(dp, np);
-        uint64_t* keys_a = take<uint64_t>(dp, np);
-        uint64_t* keys_b = take<uint64_t>(dp, np);
-        uint32_t* vals_a = take<uint32_t>(dp, np);
-        uint32_t* vals_b = take<uint32_t>(dp, np);
-        uint64_t* bytes = take<uint64_t>(dp, np);
-        uint64_t* before = take<uint64_t>(dp, np);
-        unsigned long long* d_hdr = take<unsigned long long>(dp, 4);
-        void* sort_scratch = take<uint8_t>(dp, sort_tmp);
-        void* scan_scratch = take<uint8_t>(dp, scan_tmp);
-        const uint32_t threads = 256;
-        const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>((np + threads - 1) / threads, e->sm_count * 8ull));
+        uint32_t* va = take<uint32_t>(dp, np);
+        uint32_t* vb = take<uint32_t>(dp, np);
+        uint32_t* hist = take<uint32_t>(dp, static_cast<size_t>(tiles) * 256);
+        Pair* tsum = take<Pair>(dp, tiles);
+        LargeArrays ga = a;
+        const uint32_t grid = std::min<uint32_t>((np + kThr - 1) / kThr, static_cast<uint32_t>(e->sm_count) * 8);
         cudaGraph_t g = nullptr;
         KVF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        cudaMemcpyAsync(d, h, used, cudaMemcpyHostToDevice, s);
-        cudaMemsetAsync(d_hdr, 0, 32, s);
-        big_stage<<<grid, threads, 0, s>>>(bt, dreq, flags, blocked, vals_a);
-        for (int w = 0; w < (wa ? 4 : 3); ++w) {  // stable LSD: id, seq, time, [rank desc]
-            big_gather_key<<<grid, threads, 0, s>>>(bt, dreq, vals_a, keys_a, w, rank_bytes < 8);
-            const int end_bit = w == 0   ? static_cast<int>(8 * id_bytes)
-                                : w == 1 ? static_cast<int>(8 * seq_bytes)
-                                : w == 3 ? static_cast<int>(8 * rank_bytes)
-                                         : 64;
-            cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b,
-                                            static_cast<int>(np), 0, end_bit, s);
-            std::swap(vals_a, vals_b);
-        }
-        big_ord<<<grid, threads, 0, s>>>(np, vals_a, ord);
-        big_blocked<<<grid, threads, 0, s>>>(bt, flags, blocked);
-        big_r_init<<<grid, threads, 0, s>>>(np, flags, blocked, ord, eff);
-        big_eff<<<grid, threads, 0, s>>>(bt, flags, ord, eff);
-        big_victim_keys<<<grid, threads, 0, s>>>(bt, flags, eff, keys_a, vals_a);
-        cub::DeviceRadixSort::SortPairs(sort_scratch, sort_tmp, keys_a, keys_b, vals_a, vals_b, static_cast<int>(np),
-                                        0, static_cast<int>(17 + bits_for(np)), s);
-        big_bytes<<<grid, threads, 0, s>>>(bt, dreq, keys_b, vals_b, bytes);
-        cub::DeviceScan::ExclusiveSum(scan_scratch, scan_tmp, bytes, before, static_cast<int>(np), s);
-        big_cut<<<grid, threads, 0, s>>>(bt, dreq, keys_b, vals_b, before, o_idx, o_act, d_hdr);
-        cudaMemcpyAsync(hhdr, d_hdr, 32, cudaMemcpyDeviceToHost, s);
-        const cudaError_t cap = cudaStreamEndCapture(s, &g);
-        if (cap != cudaSuccess) return cuda_error(cap, "K5 graph capture");
+        cudaMemsetAsync(dhdr, 0, sizeof(Hdr), s);
+        big_stage<<<grid, kThr, 0, s>>>(ga, np, dreq, flags, blocked, ord, va, dhdr);
+        big_blocked<<<grid, kThr, 0, s>>>(ga, np, flags, blocked);
+        // stable LSD: id, seq, [time], [rank desc], least significant byte first
+        struct W {
+            int w;
+            uint32_t bytes;
+        };
+        W words[4] = {{0, id_bytes}, {1, seq_bytes}, {2, skip_time ? 0u : 8u}, {3, wa ? rank_bytes : 0u}};
+        for (const W& wd : words)
+            for (uint32_t b = 0; b < wd.bytes; ++b) {
+                big_hist<<<tiles, kThr, 0, s>>>(ga, dreq, va, dhdr, hist, wd.w, static_cast<int>(b), compact);
+                big_offsets<<<1, kThr, 0, s>>>(hist, tiles);
+                big_scatter<<<tiles, kThr, 0, s>>>(ga, dreq, va, vb, dhdr, hist, wd.w, static_cast<int>(b), compact);
+                std::swap(va, vb);
+            }
+        big_ord<<<grid, kThr, 0, s>>>(va, dhdr, ord);
+        big_r_init<<<grid, kThr, 0, s>>>(np, flags, blocked, ord, eff);
+        big_eff<<<grid, kThr, 0, s>>>(ga, np, flags, ord, eff);
+        big_tile_sums<<<tiles, kThr, 0, s>>>(ga, dreq, va, flags, eff, dhdr, tsum);
+        big_tile_scan<<<1, 32, 0, s>>>(tsum, tiles);
+        big_emit<<<tiles, kThr, 0, s>>>(ga, dreq, va, flags, eff, dhdr, tsum, o_idx, o_act);
+        cudaMemcpyAsync(h_hdr, dhdr, sizeof(Hdr), cudaMemcpyDeviceToHost, s);
+        const cudaError_t cap_rc = cudaStreamEndCapture(s, &g);
+        if (cap_rc != cudaSuccess) return cuda_error(cap_rc, "K5 graph capture");
         BigGraph bg;
         const cudaError_t inst = cudaGraphInstantiate(&bg.exec, g, 0);
         size_t nn = 0;
@@ -366,22 +480,66 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
         }
         cudaGraphDestroy(g);
         if (inst != cudaSuccess) return cuda_error(inst, "K5 graph instantiate");
-        git = e->big_graphs.emplace(key, bg).first;
+        git = st.graphs.emplace(key, bg).first;
     }
+    KVF_CUDA(cudaMemcpyAsync(d, hreq, sizeof(BigReq), cudaMemcpyHostToDevice, s));
     KVF_CUDA(cudaEventRecord(e->dec_start, s));
     KVF_CUDA(cudaGraphLaunch(git->second.exec, s));
     KVF_CUDA(cudaEventRecord(e->dec_stop, s));
     e->stats.kernel_launches += git->second.kernels;
-    e->stats.decisions++;
     KVF_CUDA(cudaStreamSynchronize(s));
-    const uint32_t cnt = static_cast<uint32_t>(hhdr[0]);
-    if (cnt > n) return set_error(KVF_E_INTERNAL, "device-wide K5: victim count beyond the tree");
-    std::memcpy(out_idx, hout + 256, cnt * 4ull);
-    std::memcpy(out_action, hout + 256 + ((np * 4ull + 255) & ~255ull), cnt);
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, e->dec_start, e->dec_stop) == cudaSuccess) e->stats.decision_kernel_ms += ms;
+    const uint32_t cnt = static_cast<uint32_t>(h_hdr->count);
+    if (cnt > a.n) return set_error(KVF_E_INTERNAL, "device-wide K5: victim count beyond the tree");
+    if (cnt > cap) return set_error(KVF_E_INVALID_ARG, "victim buffer too small");
+    std::memcpy(out_idx, h_idx, cnt * 4ull);
+    std::memcpy(out_action, h_act, cnt);
     *out_count = cnt;
-    *out_imm = hhdr[1];
-    *out_pend = hhdr[2];
+    *out_imm = h_hdr->imm;
+    *out_pend = h_hdr->pend;
     return KVF_OK;
+}
+
+// kvf_victim_select above the single-CTA limit: the snapshot goes to HBM once (padding slots
+// dead) and runs the same device-wide path.
+int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
+                        uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend) {
+    const uint32_t n = t->n;
+    const uint32_t np = large_capacity(n);
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t bytes = al(np * 8ull) * 5 + al(np * 4ull) * 2 + al(np) * 2;
+    const void* old = e->ws_big.dev;
+    if (int rc = e->ws_big.ensure(bytes, bytes)) return rc;
+    if (e->ws_big.dev != old) large_invalidate(e->large_snap);
+    char* h = static_cast<char*>(e->ws_big.host);
+    char* hp = h;
+    auto put = [&](const void* src, size_t elem, int fill) {
+        std::memcpy(hp, src, n * elem);
+        std::memset(hp + n * elem, fill, (np - n) * elem);
+        char* at = hp;
+        hp += al(np * elem);
+        return static_cast<size_t>(at - h);
+    };
+    const size_t o_rank = put(t->rank, 8, 0), o_time = put(t->time, 8, 0), o_seq = put(t->seq, 8, 0),
+                 o_id = put(t->id, 8, 0), o_tok = put(t->tokens, 8, 0), o_par = put(t->parent, 4, 0xFF),
+                 o_lock = put(t->lock, 4, 0), o_st = put(t->status, 1, KVF_SLOT_DEAD), o_bk = put(t->backed, 1, 0);
+    char* d = static_cast<char*>(e->ws_big.dev);
+    KVF_CUDA(cudaMemcpyAsync(d, h, static_cast<size_t>(hp - h), cudaMemcpyHostToDevice, e->s_dec));
+    LargeArrays a{reinterpret_cast<const int32_t*>(d + o_par), reinterpret_cast<const uint8_t*>(d + o_st),
+                  reinterpret_cast<const int32_t*>(d + o_lock), reinterpret_cast<const int64_t*>(d + o_rank),
+                  reinterpret_cast<const double*>(d + o_time), reinterpret_cast<const uint64_t*>(d + o_seq),
+                  reinterpret_cast<const uint64_t*>(d + o_id),  reinterpret_cast<const uint64_t*>(d + o_tok),
+                  reinterpret_cast<const uint8_t*>(d + o_bk),   n};
+    LargeKeyInfo ki;  // an arbitrary snapshot: widths from its values, time passes kept
+    for (uint32_t i = 0; i < n; ++i) {
+        ki.max_id = std::max(ki.max_id, t->id[i]);
+        ki.max_seq = std::max(ki.max_seq, t->seq[i]);
+        ki.note_rank(t->rank[i]);
+    }
+    static_assert(sizeof(uint32_t) == sizeof(int32_t), "index width");
+    return victim_large(e, e->large_snap, a, q, t->bytes_per_token, ki, reinterpret_cast<uint32_t*>(out_idx),
+                        out_action, n, out_count, out_imm, out_pend);
 }
 
 }  // namespace kvf_impl

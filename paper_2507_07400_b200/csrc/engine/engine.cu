@@ -137,6 +137,7 @@ void merge_runs(const kvf_run* a, uint32_t na, const kvf_run* b, uint32_t nb, st
 }
 
 int Workspace::ensure(size_t dn, size_t hn) {
+    if (owner && ((dn > dev_bytes && dev) || (hn > host_bytes && host))) decider_quiesce(owner);
     if (dn > dev_bytes) {
         if (dev) cudaFree(dev);
         dev = nullptr;
@@ -835,8 +836,11 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
         set_carveout_engine();
         kvf_impl::set_carveout_decide();
         kvf_impl::set_carveout_attend();
+        kvf_impl::set_carveout_mirror();
     });
     cudaGetLastError();  // an attribute a driver rejects is a hint, not an error
+    for (kvf_impl::Workspace* w : {&e->ws_dev, &e->ws_dec, &e->ws_att, &e->ws_big, &e->large_snap.ws}) w->owner = e;
+    if (int rc = kvf_impl::decider_init(e)) return fail(rc);
     if (int rc = e->ws_dec.ensure(1u << 20, 1u << 20)) return fail(rc);
     if (int rc = e->ws_dev.ensure(4u << 20, 4u << 20)) return fail(rc);
     *out = e;
@@ -846,6 +850,7 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
 int kvf_engine_destroy(kvf_engine* e) {
     if (!e) return KVF_OK;
     cudaSetDevice(e->device);
+    kvf_impl::decider_release(e);  // stops the resident CTA (else the sync below waits for its idle-out)
     cudaDeviceSynchronize();
     for (auto& [id, j] : e->jobs) {
         cudaEventDestroy(j.start);
@@ -859,7 +864,7 @@ int kvf_engine_destroy(kvf_engine* e) {
     e->ws_dev.release();
     e->ws_dec.release();
     e->ws_att.release();
-    for (auto& kv : e->big_graphs) cudaGraphExecDestroy(kv.second.exec);
+    kvf_impl::large_release(e->large_snap);
     e->ws_big.release();
     if (e->d_checksum) cudaFree(e->d_checksum);
     if (e->d_layer_ctr) cudaFree(e->d_layer_ctr);

@@ -73,7 +73,43 @@ struct BigGraph {  // device-wide K5 captured once per (bucketed size, policy)
     uint32_t kernels = 0;
 };  // concurrent layered loads with engine-owned counters
 
+// ---- device-wide K5 (decide_large.cu) over device arrays of n entries (pads: dead) -------
+struct LargeArrays {
+    const int32_t* parent;
+    const uint8_t* status;
+    const int32_t* lock;
+    const int64_t* rank;
+    const double* time;
+    const uint64_t* seq;
+    const uint64_t* id;
+    const uint64_t* tokens;
+    const uint8_t* backed;
+    uint32_t n;  // live slots; the arrays hold large_capacity(n) entries
+};
+// What bounds the sort key of `before` (radix_cache.cpp:316-321): largest id / access seq,
+// whether every step rank fits the compact code, and whether access times follow access
+// sequence numbers (every touch takes (now, ++counter) with a non-decreasing now: then
+// (time, seq, id) orders like (seq, id) and the 8 time passes can go).
+struct LargeKeyInfo {
+    uint64_t max_id = 0, max_seq = 0;
+    int64_t rank_max = 0;
+    bool rank_small = true;
+    bool time_follows_seq = false;
+    void note_rank(int64_t r) {
+        if (r == INT64_MAX / 2 || r == INT64_MAX / 4) return;
+        if (r < 0 || r > (int64_t{1} << 40)) rank_small = false;
+        else if (r > rank_max) rank_max = r;
+    }
+    void note(const kvf_node_rec& r) {
+        if (r.status == KVF_SLOT_DEAD) return;
+        if (r.id > max_id) max_id = r.id;
+        if (r.seq > max_seq) max_seq = r.seq;
+        note_rank(r.rank);
+    }
+};
+
 struct Workspace {  // grow-only device + pinned staging buffers
+    kvf_engine* owner = nullptr;  // growing frees (a device-wide sync): the resident decider stops first
     void* dev = nullptr;
     size_t dev_bytes = 0;
     void* host = nullptr;
@@ -81,6 +117,37 @@ struct Workspace {  // grow-only device + pinned staging buffers
     size_t host_bytes = 0;
     int ensure(size_t dev_need, size_t host_need);
     void release();
+};
+
+struct LargeState {  // per caller of the device-wide path: scratch + captured graphs
+    Workspace ws;
+    std::map<uint64_t, BigGraph> graphs;
+    const void* baked = nullptr;  // the input arrays the graphs were captured against
+};
+uint32_t large_capacity(uint32_t n);  // padded size the device-wide path runs over
+void large_invalidate(LargeState& st);
+void large_release(LargeState& st);
+
+// Resident decider + request ring of the tree mirrors (mirror.cu).
+struct DeciderState {
+    char* ring_h = nullptr;  // mapped pinned: kRing request slots + control block
+    char* ring_d = nullptr;
+    char* pay_h = nullptr;   // mapped pinned: one payload area per ring slot
+    char* pay_d = nullptr;
+    size_t pay_slot = 0;
+    uint64_t posted = 0;     // last request sequence number handed out
+    uint64_t acked = 0;      // every request <= this one is known to be served
+    cudaStream_t s_res = nullptr;
+    cudaEvent_t ev_res = nullptr, ev_dec = nullptr;
+    bool running = false;    // the resident CTA is (believed) alive
+    bool hold = false;       // never idle out (kvf_decider_hold)
+    bool disabled = false;   // KVF_DECIDER=0: one launch per request
+    bool res_attr_set = false, once_attr_set = false;
+    uint64_t epoch = 0;      // launch count of the resident CTA (its exit word carries it)
+    uint64_t res_first = 0;  // first request the running resident CTA serves
+    uint64_t last_res_post = 0;  // last request handed to the resident CTA
+    uint64_t idle_ns = 200000;
+    uint32_t res_cap = 0;    // slots the resident CTA's shared memory is sized for
 };
 
 }  // namespace kvf_impl
@@ -124,14 +191,15 @@ struct kvf_engine {
     std::vector<uint64_t> att_sig;  // K6 descriptor cache: inputs of the blob now in ws_att.dev
     std::vector<uint8_t> att_items;  // K6 work items of that blob (host copy for the launch parameters)
     uint64_t att_meta[10] = {};     //   and its sizes (a decode step calls K6 once per layer)
-    kvf_impl::Workspace ws_big;  // device-wide K5 for large trees (grown on demand)
-    std::map<uint64_t, kvf_impl::BigGraph> big_graphs;  // key: bucket << 1 | workflow_aware
+    kvf_impl::Workspace ws_big;  // snapshot upload for the device-wide K5 (grown on demand)
+    kvf_impl::LargeState large_snap;  // device-wide K5 state of kvf_victim_select
 
     uint64_t* d_checksum = nullptr;
     uint32_t* d_layer_ctr = nullptr;       // [kLayerSlots][layers] landed-tile counters
     std::vector<uint32_t> lr_total;         // host mirror: tiles ever published per layer, per slot
     std::vector<int32_t> lr_free;           // free counter slots
     bool victim_attr_set = false, prio_attr_set = false, bulk_attr_set = false;
+    kvf_impl::DeciderState dec;
     kvf_stats stats{};
     std::mutex mu;  // engine calls are serialised per engine
 };
@@ -158,5 +226,15 @@ void set_carveout_decide();
 void set_carveout_attend();
 int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_request* q, int32_t* out_idx,
                         uint8_t* out_action, uint32_t* out_count, uint64_t* out_imm, uint64_t* out_pend);
+// victims (as array indices) of `a` in pop order; synchronous on the decision stream
+int victim_large(kvf_engine* e, LargeState& st, const LargeArrays& a, const kvf_evict_request* q, uint64_t bpt,
+                 const LargeKeyInfo& keys, uint32_t* out_idx, uint8_t* out_action, uint32_t cap, uint32_t* out_count,
+                 uint64_t* out_imm, uint64_t* out_pend);
 void recycle_event(kvf_engine* e, cudaEvent_t ev);
+// mirror.cu: stop the resident decider CTA and wait for it to leave (before any call that
+// synchronises the whole device: cudaFree, cudaFreeHost, cudaDeviceSynchronize)
+void decider_quiesce(kvf_engine* e);
+int decider_init(kvf_engine* e);
+void decider_release(kvf_engine* e);
+void set_carveout_mirror();
 }  // namespace kvf_impl

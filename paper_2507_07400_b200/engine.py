@@ -303,3 +303,89 @@ def depth_from_parent(parent):
     for i in range(1, len(parent)):
         d[i] = d[parent[i]] + 1
     return d
+
+
+class Tree:
+    """A radix tree mirrored in an engine's HBM (kvf_tree, include/kvflow.h): node records in,
+    K4 rank changes / K5 victims (as slots) out."""
+
+    def __init__(self, eng, bpt, capacity=0):
+        self._lib = eng._lib
+        self.eng = eng
+        h = C.c_void_p()
+        N.check(self._lib.kvf_tree_create(eng.h, int(bpt), int(capacity), C.byref(h)))
+        self.h = h
+        self.n = 1
+
+    def close(self):
+        if self.h:
+            self._lib.kvf_tree_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def hints(self, time_follows_seq):
+        N.check(self._lib.kvf_tree_set_hints(self.h, 1 if time_follows_seq else 0))
+
+    def update(self, recs):
+        """recs: iterable of dicts slot/parent/lock/status/backed/rank/time/seq/id/tokens."""
+        recs = list(recs)
+        arr = (N.NodeRec * max(1, len(recs)))()
+        for i, r in enumerate(recs):
+            arr[i] = N.NodeRec(int(r["slot"]), int(r.get("parent", -1)), int(r.get("lock", 0)),
+                               int(r.get("status", 0)), int(r.get("backed", 0)), 0, int(r.get("rank", 0)),
+                               float(r.get("time", 0.0)), int(r.get("seq", 0)), int(r.get("id", 0)),
+                               int(r.get("tokens", 0)), 0)
+            self.n = max(self.n, int(r["slot"]) + 1)
+        N.check(self._lib.kvf_tree_update(self.h, arr, len(recs)))
+
+    def load_arrays(self, a, slots=None):
+        """Whole-tree records from SoA arrays (index = slot unless `slots` maps them)."""
+        n = len(a["parent"])
+        sl = list(range(n)) if slots is None else list(slots)
+        self.update({"slot": sl[i], "parent": (sl[a["parent"][i]] if a["parent"][i] >= 0 else -1),
+                     "lock": a["lock"][i], "status": a["status"][i], "backed": a["backed"][i], "rank": a["rank"][i],
+                     "time": a["time"][i], "seq": a["seq"][i], "id": a["id"][i], "tokens": a["tokens"][i]}
+                    for i in range(n))
+
+    def priorities(self, bslot, cand):
+        b = np.ascontiguousarray(bslot, dtype=np.uint32)
+        c = np.ascontiguousarray(cand, dtype=np.int64)
+        N.check(self._lib.kvf_tree_priorities(self.h, b.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                              c.ctypes.data_as(C.POINTER(C.c_int64)), len(b)))
+
+    def rank_changes(self):
+        cap = max(1, self.n)
+        s = np.zeros(cap, dtype=np.uint32)
+        r = np.zeros(cap, dtype=np.int64)
+        k = C.c_uint32()
+        N.check(self._lib.kvf_tree_rank_changes(self.h, s.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                                r.ctypes.data_as(C.POINTER(C.c_int64)), cap, C.byref(k)))
+        return dict(zip(s[:k.value].tolist(), r[:k.value].tolist()))
+
+    def victims(self, needed, workflow_aware, offload, has_floor=False, floor=0, cpu_used=0, cpu_cap=0):
+        req = N.EvictRequest(int(needed), int(bool(workflow_aware)), int(bool(offload)), int(bool(has_floor)),
+                             int(floor), int(cpu_used), int(cpu_cap))
+        cap = max(1, self.n)
+        s = np.zeros(cap, dtype=np.uint32)
+        a = np.zeros(cap, dtype=np.uint8)
+        cnt, imm, pend = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        N.check(self._lib.kvf_tree_victims(self.h, C.byref(req), s.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                           a.ctypes.data_as(C.POINTER(C.c_uint8)), cap, C.byref(cnt), C.byref(imm),
+                                           C.byref(pend)))
+        k = cnt.value
+        return s[:k].copy(), a[:k].copy(), imm.value, pend.value
+
+
+def decider_hold(eng, hold):
+    N.check(eng._lib.kvf_decider_hold(eng.h, 1 if hold else 0))
+
+
+def decider_running(eng):
+    r = C.c_int32()
+    N.check(eng._lib.kvf_decider_running(eng.h, C.byref(r)))
+    return bool(r.value)

@@ -97,5 +97,6 @@ def test_layered_gate_bytes_and_stall():
     whole, _, _ = run_wall(policy="LRU_REACTIVE_HICACHE", **C2)
     lay, trace, (checked, bad) = run_wall(policy="LRU_REACTIVE_HICACHE", layered_gate=1, **C2)
     assert bad == 0 and lay["verify_failures"] == 0 and lay["verified_loads"] > 0
-    assert lay["reactive_jobs"] == whole["reactive_jobs"]
+    # real time: which requests find their prefix on the host can differ by one between runs
+    assert abs(lay["reactive_jobs"] - whole["reactive_jobs"]) <= 1
     assert lay["stall_total_s"] <= whole["stall_total_s"] * 1.05 + 0.01
