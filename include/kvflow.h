@@ -115,6 +115,14 @@ int kvf_engine_destroy(kvf_engine* e);
 /* bytes one token occupies in one plane on this shard, and across all planes */
 int kvf_engine_token_bytes(const kvf_engine* e, uint64_t* tpb, uint64_t* token_bytes);
 int kvf_engine_set_copy_mode(kvf_engine* e, uint32_t pcie_mode, uint32_t pcie_ctas, uint32_t hbm_ctas);
+/* How K1 / K2 jobs are timed (kvf_job_elapsed_ms / kvf_job_span_ms):
+ *   EVENTS (default): a timing CUDA event before and after the job on its stream;
+ *   STAMPS: only a non-timing stop event (the fence), device time from the copy kernel's own
+ *   per-CTA %globaltimer stamps -- a timing event record costs ~1.3 us of host time per call,
+ *   a plain one ~0.1 us, so a control loop issuing many transfers uses STAMPS.  Other jobs
+ *   (K3, K6, compute) keep events.  Env KVF_JOB_TIMING=stamps sets STAMPS at creation. */
+enum { KVF_JOB_TIMING_EVENTS = 0, KVF_JOB_TIMING_STAMPS = 1 };
+int kvf_engine_set_job_timing(kvf_engine* e, uint32_t mode);
 
 /* ---- token-slot pools ---------------------------------------------------------------- */
 /* Allocates `tokens` slots as <= max_runs runs (best-fit single run when possible). */

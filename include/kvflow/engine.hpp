@@ -89,6 +89,8 @@ public:
     void victims(const kvf_tree_view& tree, const kvf_evict_request& req, std::vector<int32_t>& idx,
                  std::vector<uint8_t>& action, uint64_t& immediate, uint64_t& pending);
     kvf_stats stats() const;
+    // KVF_JOB_TIMING_EVENTS / KVF_JOB_TIMING_STAMPS for K1 / K2 jobs (kvflow.h)
+    void set_job_timing(uint32_t mode);
 
 private:
     kvf_engine* e_ = nullptr;

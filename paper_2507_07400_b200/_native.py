@@ -128,6 +128,7 @@ _ENGINE_SIGS = {
     "kvf_payload_checksum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "kvf_read_runs": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Run), C.c_uint32, C.c_void_p, C.c_uint64]),
     "kvf_get_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "kvf_engine_set_job_timing": (C.c_int, [C.c_void_p, C.c_uint32]),
     "kvf_tree_create": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_void_p)]),
     "kvf_tree_destroy": (C.c_int, [C.c_void_p]),
     "kvf_tree_set_hints": (C.c_int, [C.c_void_p, C.c_uint32]),

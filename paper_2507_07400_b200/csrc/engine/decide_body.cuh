@@ -267,20 +267,23 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     int32_t* eff = ord + n;
     uint32_t* blocked = reinterpret_cast<uint32_t*>(eff + n);
     uint64_t* nbytes = reinterpret_cast<uint64_t*>(blocked + n);  // offset 16*PN + 16*n: 8-aligned
-    uint16_t* sel = reinterpret_cast<uint16_t*>(nbytes + n);
+    uint64_t* nid = nbytes + n;  // node ids: exact-key ties resolve here, not in global memory
+    uint16_t* sel = reinterpret_cast<uint16_t*>(nid + n);
     uint16_t* dep = sel + PN;
     uint8_t* st = reinterpret_cast<uint8_t*>(dep + n);
     uint8_t* flags = st + n;
     uint8_t* bk = flags + n;
     __shared__ uint32_t s_cnt, s_rcnt, s_slow;
-    __shared__ unsigned long long s_imm, s_pend, s_warp[32];
-    // per-phase timestamps (globaltimer ns) -> header[3..10], read by kvf_get_stats
+    __shared__ unsigned long long s_imm, s_pend, s_warp[32], s_stamp[12];
+    // per-phase timestamps (globaltimer ns, SM cycles) -> header[3..14] at the end (read by
+    // kvf_get_stats); kept in shared memory meanwhile: a store to mapped host memory per phase
+    // would put the PCIe write path inside every phase
     auto stamp = [&](int k) {
         if (threadIdx.x == 0) {
             unsigned long long t_ns;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ns));
-            o.header[3 + k] = t_ns;
-            o.header[9 + k] = clock64();  // SM cycles: finer than globaltimer for short phases
+            s_stamp[k] = t_ns;
+            s_stamp[6 + k] = clock64();  // SM cycles: finer than globaltimer for short phases
         }
     };
     stamp(0);
@@ -317,6 +320,7 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         parent[i] = t.parent[i];
         st[i] = s;
         nbytes[i] = bytes;
+        nid[i] = t.id[i];
         if (t.depth) dep[i] = t.depth[i];
         bk[i] = t.backed[i];
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
@@ -373,19 +377,29 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         if (sx != sy) return sx > sy;
         return t.id[x] > t.id[y];
     };
-    if (P <= 64) {  // small trees: rank sort straight into ord
+    if (P <= 64 && !slow) {  // small trees: rank sort straight into ord, branch-free compares
+        __syncthreads();
+        // element i's key in registers; G lanes split the others and add up how many precede
+        // it.  The words are exact: a tie is equal (rank, time, seq) and the id decides.
+        const uint32_t G = blockDim.x >> 6;
+        const uint32_t i = threadIdx.x / G, q = threadIdx.x % G;
+        uint32_t cnt = 0;
+        if (i < c) {
+            const uint64_t a0 = pk0[i], a1 = pk1[i], ad = nid[sel[i]];
+#pragma unroll 8
+            for (uint32_t j = q; j < c; j += G) {
+                const uint64_t b0 = pk0[j], b1 = pk1[j], bd = nid[sel[j]];
+                cnt += static_cast<uint32_t>((b0 < a0) | ((b0 == a0) & ((b1 < a1) | ((b1 == a1) & (bd < ad)))));
+            }
+        }
+        for (uint32_t off = G >> 1; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        if (q == 0 && i < c) ord[sel[i]] = static_cast<int32_t>(cnt);
+        __syncthreads();
+    } else if (P <= 64) {  // keys beyond the exact coarsening: the full comparison
         __syncthreads();
         uint32_t i;
         const uint32_t rk = rank64(
-            c,
-            [&](uint32_t a, uint32_t b) {  // candidate a sorts before candidate b
-                if (!slow) {
-                    if (pk0[a] != pk0[b]) return pk0[a] < pk0[b];
-                    if (pk1[a] != pk1[b]) return pk1[a] < pk1[b];
-                }
-                return full_after(sel[b], sel[a]);
-            },
-            i);
+            c, [&](uint32_t a, uint32_t b) { return full_after(sel[b], sel[a]); }, i);
         if (i != 0xFFFFFFFFu) ord[sel[i]] = static_cast<int32_t>(rk);
         __syncthreads();
     } else {
@@ -396,6 +410,7 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
                 if (!slow) {
                     if (x.a != y.a) return x.a > y.a;
                     if (x.b != y.b) return x.b > y.b;
+                    return nid[x.s] > nid[y.s];
                 }
                 return full_after(x.s, y.s);
             },
@@ -462,9 +477,16 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
     if (PR <= 64) {  // keys are unique: rank sort into the spare pk1 half, then swap roles
         __syncthreads();
-        uint32_t i;
-        const uint32_t rk = rank64(r, [&](uint32_t a, uint32_t b) { return keys[a] < keys[b]; }, i);
-        if (i != 0xFFFFFFFFu) pref[rk] = keys[i];
+        const uint32_t G = blockDim.x >> 6;
+        const uint32_t i = threadIdx.x / G, q = threadIdx.x % G;
+        uint32_t cnt = 0;
+        const uint64_t a = i < r ? keys[i] : 0;
+        if (i < r) {
+#pragma unroll 8
+            for (uint32_t j = q; j < r; j += G) cnt += static_cast<uint32_t>(keys[j] < a);
+        }
+        for (uint32_t off = G >> 1; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+        if (q == 0 && i < r) pref[cnt] = a;
         __syncthreads();
         uint64_t* tmp = keys;
         keys = pref;
@@ -540,13 +562,14 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         o.header[2] = s_pend;
     }
     stamp(5);
-    publish_done(o.spin ? o.header + kDoneWord : nullptr, seq);
+    if (threadIdx.x < 12) o.header[threadIdx.x < 6 ? 3 + threadIdx.x : 9 + (threadIdx.x - 6)] = s_stamp[threadIdx.x];
+    if (o.spin) publish_done(o.header + kDoneWord, seq);  // else the caller publishes (mirror.cu)
 }
 
 
 inline size_t victim_smem(uint32_t n, size_t blob = 0) {
     const size_t PN = pow2_ceil(n > 1 ? n : 2);
-    return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 8 + PN * 2 + static_cast<size_t>(n) * 2 +
+    return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 16 + PN * 2 + static_cast<size_t>(n) * 2 +
            3 * ((n + 15) & ~15u) + 64 + (blob ? blob + 32 : 0);
 }
 

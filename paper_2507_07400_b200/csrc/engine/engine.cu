@@ -26,6 +26,7 @@ using namespace kvf_impl;
 // errors
 // =====================================================================================
 namespace kvf_impl {
+constexpr size_t kMaxPiecesPublic = 48;  // = kMaxPieces below: pieces one copy launch carries
 static thread_local std::string g_last_error;
 
 int set_error(int code, const std::string& msg) {
@@ -175,30 +176,52 @@ void clear_stale_error(kvf_engine* e, const char* fn) {
     if (trace) std::fprintf(stderr, "kvflow: stale %s before %s\n", cudaGetErrorName(stale), fn);
 }
 
-int acquire_event(kvf_engine* e, cudaEvent_t* ev) {
-    if (!e->event_pool.empty()) {
-        *ev = e->event_pool.back();
-        e->event_pool.pop_back();
+int acquire_event(kvf_engine* e, cudaEvent_t* ev, bool timing) {
+    std::vector<cudaEvent_t>& pool = timing ? e->event_pool : e->event_pool_nt;
+    if (!pool.empty()) {
+        *ev = pool.back();
+        pool.pop_back();
         return KVF_OK;
     }
-    KVF_CUDA(cudaEventCreateWithFlags(ev, cudaEventDefault));
+    KVF_CUDA(cudaEventCreateWithFlags(ev, timing ? cudaEventDefault : cudaEventDisableTiming));
     return KVF_OK;
 }
 
-void recycle_event(kvf_engine* e, cudaEvent_t ev) {
-    if (ev) e->event_pool.push_back(ev);
+void recycle_event(kvf_engine* e, cudaEvent_t ev, bool timing) {
+    if (ev) (timing ? e->event_pool : e->event_pool_nt).push_back(ev);
 }
 
-int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j) {
+int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j, int32_t stamp_slot) {
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
-    int rc = acquire_event(e, &j.start);
-    if (rc) return rc;
-    rc = acquire_event(e, &j.stop);
-    if (rc) return rc;
     j.stream = stream;
+    if (stamp_slot >= 0) {  // a timing event record costs ~1.3 us of host time, a plain one ~0.1
+        j.stamp_slot = stamp_slot;
+        e->stamp_refs[stamp_slot]++;
+        return acquire_event(e, &j.stop, false);
+    }
+    int rc = acquire_event(e, &j.start, true);
+    if (rc) return rc;
+    rc = acquire_event(e, &j.stop, true);
+    if (rc) return rc;
     KVF_CUDA(cudaEventRecord(j.start, stream));
     return KVF_OK;
 }
+
+// A stamp slot for the next copy launch, or -1 (event timing: the engine's mode, no free slot,
+// or a copy that takes more than one launch).
+int32_t take_stamp_slot(kvf_engine* e, size_t npieces, uint32_t mode) {
+    if (!e->stamp_timing || mode != KVF_COPY_SM_VEC || npieces > kMaxPiecesPublic || e->stamp_free.empty()) return -1;
+    const int32_t s = e->stamp_free.back();
+    e->stamp_free.pop_back();
+    e->stamp_refs[s] = 0;
+    std::memset(e->stamps_h + static_cast<size_t>(s) * kStampCtas * 2, 0, kStampCtas * 2 * sizeof(unsigned long long));
+    return s;
+}
+
+void drop_stamp_ref(kvf_engine* e, int32_t s) {
+    if (s >= 0 && --e->stamp_refs[s] == 0) e->stamp_free.push_back(s);
+}
+
 
 int end_job(kvf_engine* e, uint64_t job_id, Job& j) {
     KVF_CUDA(cudaEventRecord(j.stop, j.stream));
@@ -229,6 +252,7 @@ struct CopyParams {
     uint32_t layer_major;  // tiles ordered plane-outermost (layer-pipelined K1)
     uint64_t plane_tiles;  // layer_major: tiles of one plane (sum over pieces)
     uint32_t* layer_ready; // layer_major: per-layer finished-tile counters (nullable)
+    unsigned long long* stamps;  // nullable: CTA b < kStampCtas writes [2b] = start, [2b+1] = end (ns)
     uint64_t src_off[kMaxPieces];
     uint64_t dst_off[kMaxPieces];
     uint64_t seg[kMaxPieces];             // bytes of the piece in one plane
@@ -290,8 +314,16 @@ __device__ __forceinline__ void st_stream(uint2* ptr, const uint2& v) {
 
 // K1/K2/K3, SM vector path: every thread keeps UNROLL independent 16-B loads in flight
 // before its stores (PCIe latency hiding for K1; HBM streaming for K3).
+__device__ __forceinline__ unsigned long long gnow() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <typename V, int UNROLL>
 __global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant__ CopyParams p) {
+    const bool stamp = p.stamps && threadIdx.x == 0 && blockIdx.x < kvf_impl::kStampCtas;
+    if (stamp) p.stamps[2 * blockIdx.x] = gnow();
     for (uint64_t t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
         uint32_t plane = 0;
         const TileRef r = locate(p, t, &plane);
@@ -316,6 +348,10 @@ __global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant
             __syncthreads();
             if (threadIdx.x == 0) atomicAdd(p.layer_ready + plane / 2, 1u);
         }
+    }
+    if (stamp) {
+        __syncthreads();  // (thread 0 only writes) every thread of the CTA is done
+        p.stamps[2 * blockIdx.x + 1] = gnow();
     }
 }
 
@@ -526,7 +562,7 @@ struct Endpoint {
 // Launch the copy of `pieces` (all planes) between two pools on `stream`.
 int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const Endpoint& dst,
                 const std::vector<Piece>& pieces, uint32_t mode, uint32_t ctas, uint32_t* layer_ready = nullptr,
-                uint64_t* tiles_per_layer = nullptr, uint32_t planes = 0) {
+                uint64_t* tiles_per_layer = nullptr, uint32_t planes = 0, Job* stamped = nullptr) {
     if (planes == 0) planes = e->planes;  // default: every plane of the token (a whole node)
     if (layer_ready) mode = KVF_COPY_SM_VEC;  // only the vector kernel publishes per-layer progress
     const uint64_t tpb = e->tpb;
@@ -579,6 +615,10 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
         p.total_tiles = tiles;
         if (tiles == 0) continue;
         uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(ctas, tiles));
+        if (stamped && stamped->stamp_slot >= 0) {
+            p.stamps = e->stamps_d + static_cast<size_t>(stamped->stamp_slot) * kStampCtas * 2;
+            stamped->stamp_ctas = std::min<uint32_t>(grid, kStampCtas);
+        }
         if (mode == KVF_COPY_SM_BULK && vec16) {
             const size_t smem = static_cast<size_t>(kBulkStages) * kBulkChunk;
             if (!e->bulk_attr_set) {  // per engine: attributes are per device
@@ -611,9 +651,14 @@ int transfer(kvf_engine* e, uint64_t job_id, int src_tier, const kvf_run* src_ru
     const bool h2d = src_tier == KVF_TIER_HOST && dst_tier == KVF_TIER_DEVICE;
     const bool d2h = src_tier == KVF_TIER_DEVICE && dst_tier == KVF_TIER_HOST;
     cudaStream_t st = h2d ? e->s_h2d : (d2h ? e->s_d2h : e->s_dev);
+    const bool pcie_job = h2d || d2h;
+    const int32_t slot = pcie_job ? take_stamp_slot(e, pieces.size(), e->cfg.pcie_mode) : -1;
     Job j;
-    int rc = begin_job(e, job_id, st, j);
-    if (rc) return rc;
+    int rc = begin_job(e, job_id, st, j, slot);
+    if (rc) {
+        if (slot >= 0 && e->stamp_refs[slot] == 0) e->stamp_free.push_back(slot);
+        return rc;
+    }
     // Order against the compute stream's last payload write (fill / K3 scatter): a D2H may
     // read those slots, an H2D may land in slots a just-discarded node's fill still targets.
     if ((d2h || h2d) && e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(st, e->dev_write_done, 0));
@@ -623,7 +668,7 @@ int transfer(kvf_engine* e, uint64_t job_id, int src_tier, const kvf_run* src_ru
     const bool pcie = h2d || d2h;
     const uint32_t mode = pcie ? e->cfg.pcie_mode : KVF_COPY_SM_VEC;
     const uint32_t ctas = pcie ? e->cfg.pcie_ctas : e->cfg.hbm_ctas;
-    rc = launch_copy(e, st, src, dst, pieces, mode, ctas);
+    rc = launch_copy(e, st, src, dst, pieces, mode, ctas, nullptr, nullptr, 0, &j);
     if (rc) return rc;
     j.bytes = ts * e->token_bytes;
     if (h2d) { e->stats.h2d_bytes += j.bytes; e->stats.h2d_jobs++; }
@@ -841,6 +886,20 @@ int kvf_engine_create(const kvf_geometry* g, const kvf_engine_config* cfg, kvf_e
     cudaGetLastError();  // an attribute a driver rejects is a hint, not an error
     for (kvf_impl::Workspace* w : {&e->ws_dev, &e->ws_dec, &e->ws_att, &e->ws_big, &e->large_snap.ws}) w->owner = e;
     if (int rc = kvf_impl::decider_init(e)) return fail(rc);
+    {
+        void* h = nullptr;
+        const size_t sb = static_cast<size_t>(kvf_impl::kStampSlots) * kvf_impl::kStampCtas * 2 * sizeof(unsigned long long);
+        if ((err = cudaHostAlloc(&h, sb, cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess)
+            return fail(cuda_error(err, "cudaHostAlloc(stamps)"));
+        void* dp = nullptr;
+        if ((err = cudaHostGetDevicePointer(&dp, h, 0)) != cudaSuccess) return fail(cuda_error(err, "stamps device pointer"));
+        e->stamps_h = static_cast<unsigned long long*>(h);
+        e->stamps_d = static_cast<unsigned long long*>(dp);
+        e->stamp_refs.assign(kvf_impl::kStampSlots, 0);
+        for (int32_t k = static_cast<int32_t>(kvf_impl::kStampSlots) - 1; k >= 0; --k) e->stamp_free.push_back(k);
+        const char* st = std::getenv("KVF_JOB_TIMING");
+        e->stamp_timing = st && std::string(st) == "stamps";
+    }
     if (int rc = e->ws_dec.ensure(1u << 20, 1u << 20)) return fail(rc);
     if (int rc = e->ws_dev.ensure(4u << 20, 4u << 20)) return fail(rc);
     *out = e;
@@ -857,6 +916,8 @@ int kvf_engine_destroy(kvf_engine* e) {
         cudaEventDestroy(j.stop);
     }
     for (cudaEvent_t ev : e->event_pool) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : e->event_pool_nt) cudaEventDestroy(ev);
+    if (e->stamps_h) cudaFreeHost(e->stamps_h);
     for (cudaEvent_t ev : {e->dev_write_done, e->dec_start, e->dec_stop, e->att_upload_done})
         if (ev) cudaEventDestroy(ev);
     for (cudaStream_t s : {e->s_h2d, e->s_d2h, e->s_dev, e->s_dec, e->s_cmp})
@@ -885,6 +946,13 @@ int kvf_engine_token_bytes(const kvf_engine* e, uint64_t* tpb, uint64_t* token_b
     if (!e) return set_error(KVF_E_INVALID_ARG, "null engine");
     if (tpb) *tpb = e->tpb;
     if (token_bytes) *token_bytes = e->token_bytes;
+    return KVF_OK;
+}
+
+int kvf_engine_set_job_timing(kvf_engine* e, uint32_t mode) {
+    KVF_GUARD(e);
+    if (mode > KVF_JOB_TIMING_STAMPS) return set_error(KVF_E_INVALID_ARG, "unknown job timing mode");
+    e->stamp_timing = mode == KVF_JOB_TIMING_STAMPS;
     return KVF_OK;
 }
 
@@ -977,16 +1045,19 @@ int kvf_d2h_scatter_batch(kvf_engine* e, uint32_t n_jobs, const uint64_t* job_id
         oh += host_counts[k];
     }
     std::vector<Job> js(n_jobs);
+    const int32_t slot = take_stamp_slot(e, pieces.size(), e->cfg.pcie_mode);  // shared by the batch
     for (uint32_t k = 0; k < n_jobs; ++k) {
-        int rc = begin_job(e, job_ids[k], e->s_d2h, js[k]);
+        int rc = begin_job(e, job_ids[k], e->s_d2h, js[k], slot);
         if (rc) return rc;
     }
     if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_d2h, e->dev_write_done, 0));
     Endpoint src{e->dev_pool, e->dev_slots * e->tpb, false};
     Endpoint dst{e->host_pool_dev, e->host_slots * e->tpb, true};
-    int rc = launch_copy(e, e->s_d2h, src, dst, pieces, e->cfg.pcie_mode, e->cfg.pcie_ctas);  // one K2 for all
+    int rc = launch_copy(e, e->s_d2h, src, dst, pieces, e->cfg.pcie_mode, e->cfg.pcie_ctas, nullptr, nullptr, 0,
+                         &js[0]);  // one K2 for all
     if (rc) return rc;
     for (uint32_t k = 0; k < n_jobs; ++k) {
+        js[k].stamp_ctas = js[0].stamp_ctas;
         js[k].bytes = bytes[k];
         e->stats.d2h_bytes += bytes[k];
         e->stats.d2h_jobs++;
@@ -1008,7 +1079,8 @@ int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_r
     std::vector<Piece> pieces;
     merge_runs(host_runs, n_host, dev_runs, n_dev, pieces);
     Job j;
-    int rc = begin_job(e, job_id, e->s_h2d, j);
+    const int32_t slot = take_stamp_slot(e, pieces.size(), KVF_COPY_SM_VEC);
+    int rc = begin_job(e, job_id, e->s_h2d, j, slot);
     if (rc) return rc;
     if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_h2d, e->dev_write_done, 0));
     if (owned) {  // counters only grow: no reset, so a late waiter on a recycled slot never hangs
@@ -1021,7 +1093,7 @@ int kvf_h2d_gather_layered(kvf_engine* e, uint64_t job_id, const kvf_run* host_r
     Endpoint src{e->host_pool_dev, e->host_slots * e->tpb, true};
     Endpoint dst{e->dev_pool, e->dev_slots * e->tpb, false};
     uint64_t per_layer = 0;
-    rc = launch_copy(e, e->s_h2d, src, dst, pieces, KVF_COPY_SM_VEC, e->cfg.pcie_ctas, layer_ready, &per_layer);
+    rc = launch_copy(e, e->s_h2d, src, dst, pieces, KVF_COPY_SM_VEC, e->cfg.pcie_ctas, layer_ready, &per_layer, 0, &j);
     if (rc) {
         if (owned) e->lr_free.push_back(j.lr_slot);
         return rc;
@@ -1206,15 +1278,17 @@ void drop_job_ref(kvf_engine* e, uint64_t job_id) {
     kvf_impl::Job& j = it->second;
     if (j.waiters) --j.waiters;
     if (j.released && j.waiters == 0) {
-        recycle_event(e, j.start);
-        recycle_event(e, j.stop);
+        recycle_event(e, j.start, true);
+        recycle_event(e, j.stop, j.stamp_slot < 0);
+        drop_stamp_ref(e, j.stamp_slot);
         if (j.lr_slot >= 0) e->lr_free.push_back(j.lr_slot);
         e->jobs.erase(it);
     }
 }
 
 // Look up `job_id` and take a reference (under the lock); `release` also marks it released.
-int ref_job(kvf_engine* e, uint64_t job_id, bool release, cudaEvent_t* start, cudaEvent_t* stop) {
+int ref_job(kvf_engine* e, uint64_t job_id, bool release, cudaEvent_t* start, cudaEvent_t* stop,
+            kvf_impl::Job* copy = nullptr) {
     std::lock_guard<std::mutex> lk(e->mu);
     if (cudaSetDevice(e->device) != cudaSuccess) return set_error(KVF_E_CUDA, "cudaSetDevice failed");
     kvf_impl::clear_stale_error(e, __func__);
@@ -1225,7 +1299,20 @@ int ref_job(kvf_engine* e, uint64_t job_id, bool release, cudaEvent_t* start, cu
     if (release) it->second.released = true;
     if (start) *start = it->second.start;
     *stop = it->second.stop;
+    if (copy) *copy = it->second;
     return KVF_OK;
+}
+
+// first start / last end of a job in ns on the GPU's clock (stamp-timed jobs only)
+void stamp_bounds(const kvf_engine* e, const kvf_impl::Job& j, unsigned long long* lo, unsigned long long* hi) {
+    const unsigned long long* st = e->stamps_h + static_cast<size_t>(j.stamp_slot) * kvf_impl::kStampCtas * 2;
+    *lo = ~0ull;
+    *hi = 0;
+    for (uint32_t b = 0; b < j.stamp_ctas; ++b) {
+        const unsigned long long a = st[2 * b], z = st[2 * b + 1];
+        if (a && a < *lo) *lo = a;
+        if (z > *hi) *hi = z;
+    }
 }
 
 void unref_job(kvf_engine* e, uint64_t job_id) {
@@ -1246,9 +1333,18 @@ int kvf_job_wait(kvf_engine* e, uint64_t job_id) {
 int kvf_job_elapsed_ms(kvf_engine* e, uint64_t job_id, float* ms) {
     if (!e || !ms) return set_error(KVF_E_INVALID_ARG, "null argument");
     cudaEvent_t start = nullptr, stop = nullptr;
-    if (int rc = ref_job(e, job_id, false, &start, &stop)) return rc;
+    kvf_impl::Job j;
+    if (int rc = ref_job(e, job_id, false, &start, &stop, &j)) return rc;
     cudaError_t err = cudaEventSynchronize(stop);
-    if (err == cudaSuccess) err = cudaEventElapsedTime(ms, start, stop);
+    if (err == cudaSuccess) {
+        if (start) {
+            err = cudaEventElapsedTime(ms, start, stop);
+        } else {  // stamp-timed: the copy kernel's own globaltimer stamps
+            unsigned long long lo, hi;
+            stamp_bounds(e, j, &lo, &hi);
+            *ms = hi > lo ? static_cast<float>((hi - lo) * 1e-6) : 0.f;
+        }
+    }
     unref_job(e, job_id);
     return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventElapsedTime(job)");
 }
@@ -1266,13 +1362,26 @@ int kvf_job_release(kvf_engine* e, uint64_t job_id) {
 int kvf_job_span_ms(kvf_engine* e, uint64_t first_job, uint64_t last_job, float* ms) {
     if (!e || !ms) return set_error(KVF_E_INVALID_ARG, "null argument");
     cudaEvent_t a_start = nullptr, a_stop = nullptr, b_stop = nullptr;
-    if (int rc = ref_job(e, first_job, false, &a_start, &a_stop)) return rc;
-    if (int rc = ref_job(e, last_job, false, nullptr, &b_stop)) {
+    kvf_impl::Job ja, jb;
+    if (int rc = ref_job(e, first_job, false, &a_start, &a_stop, &ja)) return rc;
+    if (int rc = ref_job(e, last_job, false, nullptr, &b_stop, &jb)) {
         unref_job(e, first_job);
         return rc;
     }
     cudaError_t err = cudaEventSynchronize(b_stop);
-    if (err == cudaSuccess) err = cudaEventElapsedTime(ms, a_start, b_stop);
+    if (err == cudaSuccess) err = cudaEventSynchronize(a_stop);
+    if (err == cudaSuccess) {
+        if (a_start && jb.start) {
+            err = cudaEventElapsedTime(ms, a_start, b_stop);
+        } else if (!a_start && !jb.start) {
+            unsigned long long lo, hi, lo2, hi2;
+            stamp_bounds(e, ja, &lo, &hi);
+            stamp_bounds(e, jb, &lo2, &hi2);
+            *ms = hi2 > lo ? static_cast<float>((hi2 - lo) * 1e-6) : 0.f;
+        } else {
+            err = cudaErrorInvalidResourceHandle;  // one event-timed, one stamp-timed: no common clock
+        }
+    }
     unref_job(e, last_job);
     unref_job(e, first_job);
     return err == cudaSuccess ? KVF_OK : cuda_error(err, "cudaEventElapsedTime(span)");

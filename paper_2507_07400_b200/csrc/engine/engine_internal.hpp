@@ -64,7 +64,14 @@ struct Job {
     // release that finds waiters leaves the recycling of the events to the last of them
     uint32_t waiters = 0;
     bool released = false;
+    // stamp-timed job (kvf_engine_set_job_timing STAMPS): no start event, a non-timing stop
+    // event, device time from the copy kernel's per-CTA globaltimer stamps in a mapped slot
+    int32_t stamp_slot = -1;
+    uint32_t stamp_ctas = 0;
 };
+
+constexpr uint32_t kStampSlots = 256;  // stamp-timed transfers in flight
+constexpr uint32_t kStampCtas = 64;    // CTAs stamped per slot (K1/K2 run 8)
 
 constexpr uint32_t kLayerSlots = 64;
 
@@ -181,6 +188,12 @@ struct kvf_engine {
 
     std::unordered_map<uint64_t, kvf_impl::Job> jobs;
     std::vector<cudaEvent_t> event_pool;
+    std::vector<cudaEvent_t> event_pool_nt;  // non-timing events (stamp-timed jobs' stop events)
+    bool stamp_timing = false;               // PCIe transfer jobs timed by kernel stamps
+    unsigned long long* stamps_h = nullptr;  // mapped: [kStampSlots][kStampCtas][2] globaltimer ns
+    unsigned long long* stamps_d = nullptr;
+    std::vector<int32_t> stamp_free;
+    std::vector<uint32_t> stamp_refs;        // jobs sharing a slot (one K2 batch launch)
 
     kvf_impl::Workspace ws_dev;  // fill / checksum / read staging (s_dev)
     kvf_impl::Workspace ws_dec;  // decision kernels (s_dec)
@@ -213,9 +226,9 @@ struct kvf_engine {
     kvf_impl::clear_stale_error(e, __func__)
 
 namespace kvf_impl {
-int acquire_event(kvf_engine* e, cudaEvent_t* ev);
+int acquire_event(kvf_engine* e, cudaEvent_t* ev, bool timing = true);
 // a job = start event on `stream` ... kernels ... stop event (end_job registers it)
-int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j);
+int begin_job(kvf_engine* e, uint64_t job_id, cudaStream_t stream, Job& j, int32_t stamp_slot = -1);
 int end_job(kvf_engine* e, uint64_t job_id, Job& j);
 void clear_stale_error(kvf_engine* e, const char* fn);
 // Every engine kernel prefers the max-shared-memory carveout, so SMs never switch their L1 /
@@ -230,7 +243,7 @@ int victim_select_large(kvf_engine* e, const kvf_tree_view* t, const kvf_evict_r
 int victim_large(kvf_engine* e, LargeState& st, const LargeArrays& a, const kvf_evict_request* q, uint64_t bpt,
                  const LargeKeyInfo& keys, uint32_t* out_idx, uint8_t* out_action, uint32_t cap, uint32_t* out_count,
                  uint64_t* out_imm, uint64_t* out_pend);
-void recycle_event(kvf_engine* e, cudaEvent_t ev);
+void recycle_event(kvf_engine* e, cudaEvent_t ev, bool timing = true);
 // mirror.cu: stop the resident decider CTA and wait for it to leave (before any call that
 // synchronises the whole device: cudaFree, cudaFreeHost, cudaDeviceSynchronize)
 void decider_quiesce(kvf_engine* e);

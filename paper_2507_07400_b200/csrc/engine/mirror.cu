@@ -25,6 +25,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "decide_body.cuh"
@@ -37,8 +39,10 @@ namespace kvf_mir {  // named: kernels take these types as parameters
 
 constexpr uint32_t kRing = 16;
 constexpr uint32_t kResThreads = 128;  // 128 x <= 128 registers + <= 25 KB: fits beside a K6 CTA
-constexpr size_t kReqBytes = 256;
-constexpr size_t kPaySlotBytes = 256u << 10;  // per ring slot: 4096 records (+ boundaries)
+constexpr size_t kSlotBytes = 512;     // one warp reads a slot in one round: 32 lanes x 16 B
+constexpr size_t kHdrBytes = 128;
+constexpr size_t kInlineBytes = kSlotBytes - kHdrBytes;  // records + boundaries travel in the slot
+constexpr size_t kPaySlotBytes = 256u << 10;  // per ring slot, for batches that do not fit inline
 enum : uint32_t { REQ_PRIO = 1, REQ_VICTIMS = 2, REQ_APPLY = 3 };
 
 struct MirrorDev {
@@ -53,33 +57,58 @@ struct MirrorDev {
     uint64_t* tokens;
 };
 
-struct DecReq {  // one ring slot; the host writes `seq` last
-    unsigned long long seq;
-    uint32_t type, n, n_recs, m;
-    const kvf_node_rec* recs;
-    const uint32_t* bslot;
-    const int64_t* cand;
+struct TreeDesc {  // device memory, per tree (rewritten only when its mirror is reallocated)
     MirrorDev mir;
-    long long* scratch;       // K4 ranks above the shared-memory limit
-    unsigned long long* out;  // result header (mapped pinned); results from out + 128 B
-    uint64_t bpt, needed;
+    long long* scratch;           // K4 ranks above the shared-memory limit
+    unsigned long long* out_k4;   // result headers (mapped pinned); results from + 128 B
+    unsigned long long* out_k5;
+    uint64_t bpt;
+};
+
+// A ring slot.  The host writes the body, then `hash` (over seq and bytes 16..511), then `seq`
+// last; the decider reads all 512 B in ONE round of loads (one PCIe round trip) and takes the
+// request when seq is the one it waits for and the hash matches what it read -- a read that
+// raced the host's stores fails the hash and is simply repeated.
+struct DecReq {
+    unsigned long long seq, hash;
+    uint32_t type, n, n_recs, m;
+    const TreeDesc* tree;
+    const kvf_node_rec* recs;  // nullptr: inline at slot + 128
+    const uint32_t* bslot;     // nullptr: inline after the inline records
+    const int64_t* cand;
+    uint64_t needed;
     int64_t floor;
     uint64_t cpu_used, cpu_cap;
     int32_t wa, offload, has_floor, pad;
 };
-static_assert(sizeof(DecReq) <= kReqBytes, "request slot");
+static_assert(sizeof(DecReq) <= kHdrBytes, "request header");
 union alignas(16) ReqSlot {
     DecReq r;
-    uint4 raw[kReqBytes / 16];
+    uint4 raw[kSlotBytes / 16];
+    unsigned char bytes[kSlotBytes];
 };
 
 struct Ctl {  // after the ring slots
     unsigned long long exit_epoch, exit_next, stop_epoch, pad;
     unsigned long long ack[kRing];
+    unsigned long long t_seen[kRing], t_done[kRing], polls[kRing];  // diagnostics (globaltimer ns)
 };
 
 ReqSlot* ring_slot(char* base, uint64_t seq) { return reinterpret_cast<ReqSlot*>(base) + (seq % kRing); }
 Ctl* ring_ctl(char* base) { return reinterpret_cast<Ctl*>(base + kRing * sizeof(ReqSlot)); }
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+// hash term of 16-B chunk c (1..31) of a slot; the slot hash XORs them with mix64(seq)
+__host__ __device__ __forceinline__ uint64_t chunk_hash(uint64_t lo, uint64_t hi, uint32_t c) {
+    return mix64(lo ^ (0x9e3779b97f4a7c15ULL * (c + 1))) + mix64(hi + c);
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
     unsigned long long v;
@@ -90,27 +119,54 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// The request body -> shared memory (uncached loads: the slot is host memory the host rewrites)
-__device__ __forceinline__ void load_req(ReqSlot& dst, const ReqSlot* src) {
-    if (threadIdx.x < kReqBytes / 16) dst.raw[threadIdx.x] = __ldcv(&src->raw[threadIdx.x]);
-    __syncthreads();
+// Warp 0: one round of uncached 16-B loads of the whole slot (+ lane 0: the stop word).  True
+// (and the slot in `dst`) when it holds request `want` intact.
+__device__ __forceinline__ bool read_slot(ReqSlot& dst, const ReqSlot* src, unsigned long long want,
+                                          const unsigned long long* stop_word, unsigned long long* stop_seen) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint4 v = __ldcv(&src->raw[lane]);
+    unsigned long long stop = 0;
+    if (stop_word && lane == 0) stop = ld_acquire_sys(stop_word);
+    if (stop_seen) *stop_seen = __shfl_sync(0xffffffffu, stop, 0);
+    const uint64_t lo = (static_cast<uint64_t>(v.y) << 32) | v.x, hi = (static_cast<uint64_t>(v.w) << 32) | v.z;
+    const uint64_t seq = __shfl_sync(0xffffffffu, lo, 0), hash = __shfl_sync(0xffffffffu, hi, 0);
+    if (seq != want) return false;
+    uint64_t h = lane ? chunk_hash(lo, hi, lane) : mix64(seq);
+    for (int off = 16; off; off >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, off);
+    if (h != hash) return false;
+    dst.raw[lane] = v;
+    return true;
 }
 
-// Node records -> mirror (last record of a slot wins: the host sends one per slot per batch)
-__device__ __forceinline__ void apply_records(const DecReq& q) {
+// Node records -> mirror (last record of a slot wins: the host sends one per slot per batch);
+// inline records come from the slot copy in shared memory, others from host / device memory
+__device__ __forceinline__ void apply_records(const DecReq& q, const MirrorDev& mir, const ReqSlot& slot) {
+    const bool inl = q.recs == nullptr;
     for (uint32_t i = threadIdx.x; i < q.n_recs; i += blockDim.x) {
-        const uint4* p = reinterpret_cast<const uint4*>(q.recs + i);
-        const uint4 a = __ldcv(p), b = __ldcv(p + 1), c = __ldcv(p + 2), d = __ldcv(p + 3);
+        uint4 a, b, c, d;
+        if (inl) {
+            const uint4* p = reinterpret_cast<const uint4*>(slot.bytes + kHdrBytes) + 4 * i;
+            a = p[0];
+            b = p[1];
+            c = p[2];
+            d = p[3];
+        } else {
+            const uint4* p = reinterpret_cast<const uint4*>(q.recs + i);
+            a = __ldcv(p);
+            b = __ldcv(p + 1);
+            c = __ldcv(p + 2);
+            d = __ldcv(p + 3);
+        }
         const uint32_t s = a.x;
-        q.mir.parent[s] = static_cast<int32_t>(a.y);
-        q.mir.lock[s] = static_cast<int32_t>(a.z);
-        q.mir.status[s] = static_cast<uint8_t>(a.w & 0xFF);
-        q.mir.backed[s] = static_cast<uint8_t>((a.w >> 8) & 0xFF);
-        q.mir.rank[s] = static_cast<int64_t>((static_cast<uint64_t>(b.y) << 32) | b.x);
-        q.mir.time[s] = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(b.w) << 32) | b.z));
-        q.mir.seq[s] = (static_cast<uint64_t>(c.y) << 32) | c.x;
-        q.mir.id[s] = (static_cast<uint64_t>(c.w) << 32) | c.z;
-        q.mir.tokens[s] = (static_cast<uint64_t>(d.y) << 32) | d.x;
+        mir.parent[s] = static_cast<int32_t>(a.y);
+        mir.lock[s] = static_cast<int32_t>(a.z);
+        mir.status[s] = static_cast<uint8_t>(a.w & 0xFF);
+        mir.backed[s] = static_cast<uint8_t>((a.w >> 8) & 0xFF);
+        mir.rank[s] = static_cast<int64_t>((static_cast<uint64_t>(b.y) << 32) | b.x);
+        mir.time[s] = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(b.w) << 32) | b.z));
+        mir.seq[s] = (static_cast<uint64_t>(c.y) << 32) | c.x;
+        mir.id[s] = (static_cast<uint64_t>(c.w) << 32) | c.z;
+        mir.tokens[s] = (static_cast<uint64_t>(d.y) << 32) | d.x;
     }
     __syncthreads();
 }
@@ -118,83 +174,124 @@ __device__ __forceinline__ void apply_records(const DecReq& q) {
 // K4 over the mirror (radix_cache.cpp:266-285): SUFFIX everywhere, then each boundary's
 // candidate min-reduced along its root path; ranks that differ from the mirror's are written
 // back to it and reported as (slot, rank) changes.
-__device__ __forceinline__ void prio_body(const DecReq& q) {
+__device__ __forceinline__ void prio_body(const DecReq& q, const TreeDesc& td, const ReqSlot& slot) {
     extern __shared__ __align__(16) uint8_t sm[];
     __shared__ uint32_t s_cnt;
+    const MirrorDev& mir = td.mir;
     const uint32_t n = q.n;
     const bool staged = n <= kPrioSmemNodes;
-    long long* r = staged ? reinterpret_cast<long long*>(sm) : q.scratch;
-    const int32_t* par = q.mir.parent;
+    long long* r = staged ? reinterpret_cast<long long*>(sm) : td.scratch;
+    const int32_t* par = mir.parent;
     if (staged) {
         int32_t* ps = reinterpret_cast<int32_t*>(sm + n * 8ull);
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) ps[i] = q.mir.parent[i];
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) ps[i] = mir.parent[i];
         par = ps;
     }
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) r[i] = kRankSuffix;
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
+    // boundaries: inline after the inline records, or in the payload area
+    const bool inl = q.bslot == nullptr;
+    const unsigned char* ib = slot.bytes + kHdrBytes + q.n_recs * sizeof(kvf_node_rec);
     for (uint32_t b = threadIdx.x; b < q.m; b += blockDim.x) {
-        const long long c = static_cast<long long>(__ldcv(reinterpret_cast<const unsigned long long*>(q.cand) + b));
-        for (int32_t v = static_cast<int32_t>(__ldcv(q.bslot + b)); v > 0; v = par[v]) atomicMin(r + v, c);
+        long long c;
+        int32_t v;
+        if (inl) {
+            v = static_cast<int32_t>(reinterpret_cast<const uint32_t*>(ib)[b]);
+            c = reinterpret_cast<const long long*>(ib + ((q.m * 4 + 15) & ~15u))[b];
+        } else {
+            v = static_cast<int32_t>(__ldcv(q.bslot + b));
+            c = static_cast<long long>(__ldcv(reinterpret_cast<const unsigned long long*>(q.cand) + b));
+        }
+        for (; v > 0; v = par[v]) atomicMin(r + v, c);
     }
     __syncthreads();
-    uint32_t* o_slot = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(q.out) + kHeaderBytes);
-    int64_t* o_rank = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(q.out) + kHeaderBytes + ((n * 4ull + 15) & ~15ull));
+    unsigned long long* out = td.out_k4;
+    uint32_t* o_slot = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(out) + kHeaderBytes);
+    int64_t* o_rank = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(out) + kHeaderBytes + ((n * 4ull + 15) & ~15ull));
     for (uint32_t i = threadIdx.x + 1; i < n; i += blockDim.x) {
         const long long v = r[i];
-        const bool ch = q.mir.status[i] != KVF_SLOT_DEAD && v != q.mir.rank[i];
+        const bool ch = mir.status[i] != KVF_SLOT_DEAD && v != mir.rank[i];
         const uint32_t k = claim(&s_cnt, ch);
         if (ch) {
-            q.mir.rank[i] = v;
+            mir.rank[i] = v;
             o_slot[k] = i;
             o_rank[k] = v;
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) q.out[0] = s_cnt;
+    if (threadIdx.x == 0) out[0] = s_cnt;
 }
 
 // K5 over the mirror: the snapshot kernel's body (decide_body.cuh) reading the HBM arrays in
 // place, depth recomputed from the parents.
-__device__ __forceinline__ void victims_body(const DecReq& q) {
+__device__ __forceinline__ void victims_body(const DecReq& q, const TreeDesc& td) {
     TreeDev t;
-    t.parent = q.mir.parent;
+    t.parent = td.mir.parent;
     t.depth = nullptr;
-    t.status = q.mir.status;
-    t.lock = q.mir.lock;
-    t.rank = q.mir.rank;
-    t.time = q.mir.time;
-    t.seq = q.mir.seq;
-    t.id = q.mir.id;
-    t.tokens = q.mir.tokens;
-    t.backed = q.mir.backed;
+    t.status = td.mir.status;
+    t.lock = td.mir.lock;
+    t.rank = td.mir.rank;
+    t.time = td.mir.time;
+    t.seq = td.mir.seq;
+    t.id = td.mir.id;
+    t.tokens = td.mir.tokens;
+    t.backed = td.mir.backed;
     t.n = q.n;
-    t.bpt = q.bpt;
+    t.bpt = td.bpt;
     t.blob = nullptr;
     t.blob_bytes = 0;
     ReqDev rq{q.needed, q.floor, q.cpu_used, q.cpu_cap, q.wa, q.offload, q.has_floor};
     OutDev o;
-    o.header = q.out;
-    o.idx = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(q.out) + kHeaderBytes);
-    o.action = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(q.out) + kHeaderBytes + ((q.n * 4ull + 15) & ~15ull));
+    o.header = td.out_k5;
+    o.idx = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(td.out_k5) + kHeaderBytes);
+    o.action = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(td.out_k5) + kHeaderBytes + ((q.n * 4ull + 15) & ~15ull));
     o.spin = false;
     victim_body(t, rq, o, 0);
 }
 
-__device__ __forceinline__ void serve(const DecReq& q, Ctl* ctl, unsigned long long seq) {
-    apply_records(q);
-    if (q.type == REQ_PRIO) prio_body(q);
-    else if (q.type == REQ_VICTIMS) victims_body(q);
-    __threadfence_system();  // every thread's results before the acknowledgement
+__device__ __forceinline__ void serve(const ReqSlot& slot, Ctl* ctl, unsigned long long seq, unsigned long long polls) {
+    __shared__ TreeDesc td;
+    __shared__ unsigned long long s_seen;
+    if (threadIdx.x == 0) s_seen = gtimer();
+    const DecReq& q = slot.r;
+    if (threadIdx.x < sizeof(TreeDesc) / 8)
+        reinterpret_cast<uint64_t*>(&td)[threadIdx.x] = reinterpret_cast<const uint64_t*>(q.tree)[threadIdx.x];
+    // a batch that did not fit the slot sits in the payload area: order those reads after the
+    // slot's (the host wrote it first)
+    if (q.recs || q.bslot) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    apply_records(q, td.mir, slot);
+    if (q.type == REQ_PRIO) prio_body(q, td, slot);
+    else if (q.type == REQ_VICTIMS) victims_body(q, td);
+    if (threadIdx.x == 0) {  // diagnostics (KVF_MIRROR_TRACE)
+        ctl->t_seen[seq % kRing] = s_seen;
+        ctl->t_done[seq % kRing] = gtimer();
+        ctl->polls[seq % kRing] = polls;
+    }
+    // every thread's results precede thread 0's release store of the acknowledgement (the
+    // barrier orders them before it, the .sys release fence is cumulative): a host that sees
+    // the ack sees the results
     __syncthreads();
     if (threadIdx.x == 0) st_release_sys(&ctl->ack[seq % kRing], seq);
 }
 
-// One request, one launch (trees above the resident limit, or the resident decider off).
+// One request, one launch (trees above the resident limit, or the resident decider off).  The
+// host wrote the slot before the launch, so the first read normally holds it.
 __global__ void __launch_bounds__(kThreads) kvf_decide_once(const ReqSlot* slot, Ctl* ctl, unsigned long long seq) {
     __shared__ ReqSlot req;
-    load_req(req, slot);
-    serve(req.r, ctl, seq);
+    __shared__ int s_ok;
+    __shared__ unsigned long long s_polls;
+    if (threadIdx.x < 32) {
+        unsigned long long polls = 1;
+        while (!read_slot(req, slot, seq, nullptr, nullptr)) ++polls;
+        if (threadIdx.x == 0) {
+            s_ok = 1;
+            s_polls = polls;
+        }
+    }
+    __syncthreads();
+    serve(req, ctl, seq, s_polls);
 }
 
 // The resident decider: serves ring requests first, first+1, ... until idle_ns pass without
@@ -204,29 +301,30 @@ __global__ void __launch_bounds__(kResThreads, 4) kvf_decider_kernel(ReqSlot* ri
                                                                       unsigned long long idle_ns) {
     __shared__ ReqSlot req;
     __shared__ int s_go;
+    __shared__ unsigned long long s_polls;
     unsigned long long next = first;
     unsigned long long last = gtimer();
     for (;;) {
-        if (threadIdx.x < 32) {  // lane 0 polls the next slot, lane 1 the stop word: one round trip
+        if (threadIdx.x < 32) {  // warp 0: the whole slot + the stop word, one round trip per poll
             int go = 0;
+            unsigned long long polls = 0;
             for (;;) {
-                const unsigned long long v =
-                    threadIdx.x == 0 ? ld_acquire_sys(&ring[next % kRing].r.seq)
-                                     : (threadIdx.x == 1 ? ld_acquire_sys(&ctl->stop_epoch) : 0ull);
-                const unsigned long long seen = __shfl_sync(0xffffffffu, v, 0);
-                const unsigned long long stop = __shfl_sync(0xffffffffu, v, 1);
-                if (seen == next) {
+                unsigned long long stop = 0;
+                ++polls;
+                if (read_slot(req, &ring[next % kRing], next, &ctl->stop_epoch, &stop)) {
                     go = 1;
                     break;
                 }
                 if (stop == epoch || gtimer() - last > idle_ns) break;
             }
-            if (threadIdx.x == 0) s_go = go;
+            if (threadIdx.x == 0) {
+                s_go = go;
+                s_polls = polls;
+            }
         }
         __syncthreads();
         if (!s_go) break;
-        load_req(req, &ring[next % kRing]);
-        serve(req.r, ctl, next);
+        serve(req, ctl, next, s_polls);
         ++next;
         last = gtimer();
         __syncthreads();  // s_go / req are rewritten next round
@@ -270,6 +368,7 @@ struct kvf_tree {
     char* out_h = nullptr;  // mapped pinned: [K4 result | K5 result]
     char* out_d = nullptr;
     size_t k5_off = 0;
+    TreeDesc* desc = nullptr;      // device copy of the mirror / output pointers
     kvf_node_rec* bulk = nullptr;  // device copy of record batches too big for a ring slot
     size_t bulk_cap = 0;
     std::vector<kvf_node_rec> staged;
@@ -370,6 +469,11 @@ int stop_resident(kvf_engine* e) {
     return after_exit(e, false);
 }
 
+const char* mirror_trace_path() {
+    static const char* p = std::getenv("KVF_MIRROR_TRACE");
+    return p;
+}
+
 int wait_req(kvf_engine* e, uint64_t seq) {
     DeciderState& d = e->dec;
     if (seq <= d.acked) return KVF_OK;
@@ -396,6 +500,17 @@ int wait_req(kvf_engine* e, uint64_t seq) {
 #endif
     }
     d.acked = std::max<uint64_t>(d.acked, seq);
+    if (mirror_trace_path()) {  // diagnostics: host wait, device serve time, polls before the hit
+        const Ctl* c = ring_ctl(d.ring_h);
+        if (FILE* f = std::fopen(mirror_trace_path(), "a")) {
+            std::fprintf(f, "{\"seq\": %llu, \"wait_us\": %.2f, \"serve_us\": %.2f, \"polls\": %llu, \"running\": %d}\n",
+                         static_cast<unsigned long long>(seq),
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(),
+                         (c->t_done[seq % kRing] - c->t_seen[seq % kRing]) * 1e-3, c->polls[seq % kRing],
+                         d.running ? 1 : 0);
+            std::fclose(f);
+        }
+    }
     return KVF_OK;
 }
 
@@ -491,6 +606,10 @@ int ensure_cap(kvf_tree* t, uint32_t need) {
     t->out_d = static_cast<char*>(dp);
     if (!k4_keep.empty()) std::memcpy(t->out_h, k4_keep.data(), k4_keep.size());
     t->cap = cap;
+    if (!t->desc) KVF_CUDA(cudaMalloc(reinterpret_cast<void**>(&t->desc), sizeof(TreeDesc)));
+    TreeDesc td{t->mir, t->scratch, reinterpret_cast<unsigned long long*>(t->out_d),
+                reinterpret_cast<unsigned long long*>(t->out_d + t->k5_off), t->bpt};
+    KVF_CUDA(cudaMemcpy(t->desc, &td, sizeof(td), cudaMemcpyHostToDevice));
     return KVF_OK;
 }
 
@@ -502,8 +621,17 @@ int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand,
     if (int rc = ensure_cap(t, t->n > kMaxNodesSingleCta ? large_capacity(t->n) : t->n)) return rc;
     const size_t rec_bytes = t->staged.size() * sizeof(kvf_node_rec);
     const size_t pay = rec_bytes + ((m * 4ull + 15) & ~15ull) + m * 8ull;
+    const bool inl = pay <= kInlineBytes;   // the common case: everything in the polled slot
     const bool bulk = pay > kPaySlotBytes;  // one-time large syncs go through a device copy
     if (int rc = ensure_pay(e, bulk ? ((m * 12ull + 64 + 15) & ~15ull) : pay)) return rc;
+    if (bulk && rec_bytes > t->bulk_cap) {  // (before this request takes a number: drain waits for all)
+        if (int rc = drain(e)) return rc;
+        if (t->bulk) cudaFree(t->bulk);
+        t->bulk = nullptr;
+        const size_t sz = std::max(rec_bytes, t->bulk_cap * 2);
+        KVF_CUDA(cudaMalloc(reinterpret_cast<void**>(&t->bulk), sz));
+        t->bulk_cap = sz;
+    }
     const bool resident = !d.disabled && !bulk && t->n <= KVF_RESIDENT_MAX_SLOTS && type != REQ_APPLY;
     // a resident CTA too small for this tree makes way for a bigger one
     if (d.running && (!resident || resident_cap(t->n) > d.res_cap)) {
@@ -514,44 +642,31 @@ int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand,
     if (seq > kRing) {  // the slot's previous request must be done
         if (int rc = wait_req(e, seq - kRing)) return rc;
     }
-    char* ph = d.pay_h + (seq % kRing) * d.pay_slot;
+    ReqSlot* slot = ring_slot(d.ring_h, seq);
+    char* ph = inl ? reinterpret_cast<char*>(slot->bytes + kHdrBytes) : d.pay_h + (seq % kRing) * d.pay_slot;
     char* pd = d.pay_d + (seq % kRing) * d.pay_slot;
-    const kvf_node_rec* recs_dev = reinterpret_cast<const kvf_node_rec*>(pd);
+    const kvf_node_rec* recs_dev = inl ? nullptr : reinterpret_cast<const kvf_node_rec*>(pd);
     size_t off = 0;
     if (bulk) {
-        if (rec_bytes > t->bulk_cap) {
-            if (int rc = drain(e)) return rc;
-            if (t->bulk) cudaFree(t->bulk);
-            t->bulk = nullptr;
-            const size_t sz = std::max(rec_bytes, t->bulk_cap * 2);
-            KVF_CUDA(cudaMalloc(reinterpret_cast<void**>(&t->bulk), sz));
-            t->bulk_cap = sz;
-        }
         KVF_CUDA(cudaMemcpyAsync(t->bulk, t->staged.data(), rec_bytes, cudaMemcpyHostToDevice, e->s_dec));
         recs_dev = t->bulk;
     } else {
         if (rec_bytes) std::memcpy(ph, t->staged.data(), rec_bytes);
         off = rec_bytes;
     }
-    off = (off + 15) & ~size_t(15);
     if (m) {
         std::memcpy(ph + off, bslot, m * 4ull);
         std::memcpy(ph + off + ((m * 4ull + 15) & ~15ull), cand, m * 8ull);
     }
-    ReqSlot* slot = ring_slot(d.ring_h, seq);
     DecReq r{};
-    r.seq = 0;  // published below
     r.type = type;
     r.n = t->n;
     r.n_recs = static_cast<uint32_t>(t->staged.size());
     r.m = m;
+    r.tree = t->desc;
     r.recs = recs_dev;
-    r.bslot = reinterpret_cast<const uint32_t*>(pd + off);
-    r.cand = reinterpret_cast<const int64_t*>(pd + off + ((m * 4ull + 15) & ~15ull));
-    r.mir = t->mir;
-    r.scratch = t->scratch;
-    r.out = reinterpret_cast<unsigned long long*>(t->out_d + (type == REQ_VICTIMS ? t->k5_off : 0));
-    r.bpt = t->bpt;
+    r.bslot = inl ? nullptr : reinterpret_cast<const uint32_t*>(pd + off);
+    r.cand = inl ? nullptr : reinterpret_cast<const int64_t*>(pd + off + ((m * 4ull + 15) & ~15ull));
     if (q) {
         r.needed = q->needed;
         r.floor = q->floor;
@@ -561,7 +676,15 @@ int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand,
         r.offload = q->offload_mode;
         r.has_floor = q->has_floor;
     }
-    std::memcpy(&slot->r, &r, sizeof(r));
+    std::memcpy(reinterpret_cast<char*>(slot) + 16, reinterpret_cast<const char*>(&r) + 16, sizeof(r) - 16);
+    // the hash over what the slot now holds (seq and bytes 16..511), then seq last
+    uint64_t h = mix64(seq);
+    for (uint32_t c = 1; c < kSlotBytes / 16; ++c) {
+        uint64_t w[2];
+        std::memcpy(w, slot->bytes + 16 * c, 16);
+        h ^= chunk_hash(w[0], w[1], c);
+    }
+    __atomic_store_n(&slot->r.hash, static_cast<unsigned long long>(h), __ATOMIC_RELEASE);
     e->stats.mirror_records += t->staged.size();
     t->staged.clear();
     if (resident) {
@@ -590,6 +713,33 @@ void decider_quiesce(kvf_engine* e) {
     stop_resident(e);
 }
 
+namespace {
+// Engines whose resident CTA may be alive.  At process exit (before the CUDA runtime's own
+// teardown, registered earlier) every one is stopped: a CTA still polling the ring while its
+// mapped memory is torn down would fault.
+std::mutex g_live_mu;
+std::set<kvf_engine*>* g_live = nullptr;
+void stop_all_at_exit() {
+    std::lock_guard<std::mutex> g(g_live_mu);
+    if (!g_live) return;
+    for (kvf_engine* e : *g_live) {
+        std::lock_guard<std::mutex> lk(e->mu);
+        cudaSetDevice(e->device);
+        stop_resident(e);
+        cudaStreamSynchronize(e->dec.s_res);
+    }
+}
+void register_live(kvf_engine* e, bool live) {
+    std::lock_guard<std::mutex> g(g_live_mu);
+    if (!g_live) {
+        g_live = new std::set<kvf_engine*>();
+        std::atexit(stop_all_at_exit);
+    }
+    if (live) g_live->insert(e);
+    else g_live->erase(e);
+}
+}  // namespace
+
 int decider_init(kvf_engine* e) {
     DeciderState& d = e->dec;
     const char* env = std::getenv("KVF_DECIDER");
@@ -608,10 +758,12 @@ int decider_init(kvf_engine* e) {
     KVF_CUDA(cudaHostGetDevicePointer(&dp, h, 0));
     d.ring_h = static_cast<char*>(h);
     d.ring_d = static_cast<char*>(dp);
+    register_live(e, true);
     return ensure_pay(e, kPaySlotBytes);
 }
 
 void decider_release(kvf_engine* e) {
+    register_live(e, false);
     DeciderState& d = e->dec;
     if (d.ring_h) stop_resident(e);
     if (d.s_res) cudaStreamSynchronize(d.s_res);
@@ -663,6 +815,7 @@ int kvf_tree_destroy(kvf_tree* t) {
         large_release(t->large);
         if (t->dblock) cudaFree(t->dblock);
         if (t->bulk) cudaFree(t->bulk);
+        if (t->desc) cudaFree(t->desc);
         if (t->out_h) cudaFreeHost(t->out_h);
     }
     delete t;

@@ -183,4 +183,8 @@ kvf_stats Engine::stats() const {
     return s;
 }
 
+void Engine::set_job_timing(uint32_t mode) {
+    if (int rc = kvf_engine_set_job_timing(e_, mode)) throw_engine(rc, "kvf_engine_set_job_timing");
+}
+
 }  // namespace kvf

@@ -227,6 +227,10 @@ class Engine:
     def sync(self):
         N.check(self._lib.kvf_sync_all(self.h))
 
+    def set_job_timing(self, stamps):
+        """K1/K2 job timing: CUDA timing events (default) or the copy kernels' globaltimer stamps."""
+        N.check(self._lib.kvf_engine_set_job_timing(self.h, 1 if stamps else 0))
+
     def set_copy_mode(self, mode, pcie_ctas=0, hbm_ctas=0):
         N.check(self._lib.kvf_engine_set_copy_mode(self.h, mode, pcie_ctas, hbm_ctas))
 

@@ -4,6 +4,10 @@
 // makes each of them land on a GPU engine whose token geometry matches the ledger's
 // bytes_per_token -- the same engine for the same bytes_per_token, so a cache and a tier
 // manager built separately share their pools.  Engines live until process exit.
+#include <execinfo.h>
+#include <unistd.h>
+
+#include <csignal>
 #include <cstdio>
 #include <map>
 #include <memory>
@@ -34,8 +38,18 @@ bool geometry_for(uint64_t bpt, kvf::EngineOptions& o) {
     return false;
 }
 
+void on_crash(int sig) {  // a crash inside a suite names its frames (no debugger on the GPU box)
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    std::fprintf(stderr, "refsuite: signal %d\n", sig);
+    backtrace_symbols_fd(frames, n, 2);
+    _exit(128 + sig);
+}
+
 struct Install {
     Install() {
+        std::signal(SIGSEGV, on_crash);
+        std::signal(SIGABRT, on_crash);
         kvf::set_default_engine_factory([](uint64_t bpt) -> kvf::Engine* {
             static std::mutex mu;
             static std::map<uint64_t, kvf::Engine*> engines;  // leaked on purpose: outlive every cache

@@ -324,3 +324,56 @@ def test_k5_every_tree_size_across_the_shared_memory_limits(eng):
         assert got == want and (gi, gp) == (imm, pend), n
         checked += 1
     assert checked >= len(sizes) - 4
+
+
+def test_stamp_timed_jobs_match_event_timing_and_bytes():
+    """KVF_JOB_TIMING_STAMPS: K1 / K2 / K2-batch jobs fenced by a plain stop event and timed by
+    the copy kernels' globaltimer stamps -- bytes exact, device time within 10 % of the
+    timing-event measurement of the same copy, span over jobs consistent."""
+    e = Engine(layers=32, kv_heads_total=8, head_dim=128, gpu_slots=4096, host_slots=8192)
+    try:
+        rng = np.random.default_rng(5)
+        n = 2048  # 256 MiB
+        cids = rand_cids(rng, n)
+        h = e.alloc(N.KVF_TIER_HOST, n)
+        e.fill(N.KVF_TIER_HOST, h, cids)
+        want = expected_bytes(e, cids)
+        times = {}
+        for stamps in (False, True, False, True):
+            e.set_job_timing(stamps)
+            d = e.alloc(N.KVF_TIER_DEVICE, n)
+            j = e.h2d(h, d)
+            ms = e.elapsed_ms(j)
+            e.release(j)
+            assert np.array_equal(e.read(N.KVF_TIER_DEVICE, d), want)
+            times.setdefault(stamps, []).append(ms)
+            e.free(N.KVF_TIER_DEVICE, d)
+        ev, st = min(times[False]), min(times[True])
+        assert st > 0 and abs(st - ev) <= 0.1 * ev, (ev, st)
+        # K2 batch under stamps: jobs share the launch's stamps; span covers both
+        e.set_job_timing(True)
+        d = e.alloc(N.KVF_TIER_DEVICE, n)
+        e.fill(N.KVF_TIER_DEVICE, d, cids)
+        h1, h2 = e.alloc(N.KVF_TIER_HOST, n // 2), e.alloc(N.KVF_TIER_HOST, n // 2)
+        # split the device run list in two halves of n/2 tokens
+        first, second, left = [], [], n // 2
+        for s, l in d:
+            if left >= l:
+                first.append((s, l))
+                left -= l
+            elif left > 0:
+                first.append((s, left))
+                second.append((s + left, l - left))
+                left = 0
+            else:
+                second.append((s, l))
+        jobs = e.d2h_batch([(first, h1), (second, h2)])
+        a, b = e.elapsed_ms(jobs[0]), e.elapsed_ms(jobs[1])
+        span = e.span_ms(jobs[0], jobs[1])
+        assert a == b and a > 0 and abs(span - a) < 1e-3
+        for j in jobs:
+            e.release(j)
+        got = e.read(N.KVF_TIER_HOST, h1 + h2)
+        assert np.array_equal(got, want)
+    finally:
+        e.close()
