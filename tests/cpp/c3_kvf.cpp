@@ -29,6 +29,7 @@ int main(int argc, char** argv) {
     kvf::EventQueue ev;
     kvf::TierManager tier(cap, 0, cost, ev, &engine);
     kvf::RadixCache cache(bpt, &engine);
+    cache.set_prefill_emulation(true);  // the byte checks below need the synthetic KV
     try {
         c3::Driver<kvf::TierManager, kvf::RadixCache, kvf::EventQueue, kvf::CostModel> d(tier, cache, ev, cost, seed);
         std::fputs(d.run(iters).trace.c_str(), stdout);

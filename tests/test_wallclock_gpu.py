@@ -97,6 +97,10 @@ def test_layered_gate_bytes_and_stall():
     whole, _, _ = run_wall(policy="LRU_REACTIVE_HICACHE", **C2)
     lay, trace, (checked, bad) = run_wall(policy="LRU_REACTIVE_HICACHE", layered_gate=1, **C2)
     assert bad == 0 and lay["verify_failures"] == 0 and lay["verified_loads"] > 0
-    # real time: which requests find their prefix on the host can differ by one between runs
-    assert abs(lay["reactive_jobs"] - whole["reactive_jobs"]) <= 1
-    assert lay["stall_total_s"] <= whole["stall_total_s"] * 1.05 + 0.01
+    # Real time: which requests find their prefix on the host depends on when write-backs
+    # land, so the two runs' reactive-load counts differ (29-40 of 40 seen); compare the stall
+    # each reactive load exposes.
+    assert lay["reactive_jobs"] > 0 and whole["reactive_jobs"] > 0
+    per_lay = lay["stall_total_s"] / lay["reactive_jobs"]
+    per_whole = whole["stall_total_s"] / whole["reactive_jobs"]
+    assert per_lay <= per_whole * 1.05 + 0.5e-3, (per_lay, per_whole)
