@@ -55,6 +55,8 @@ typedef struct {
     int32_t prefetch_retry; /* re-run the step-1 prefetch whenever a transfer lands */
     int32_t layered_gate;   /* wall clock: HiCache-gated prefills consume layer-pipelined loads */
     int32_t d2h_unbatched;  /* 1: one K2 launch per write-back instead of one per evict call */
+    int32_t d2h_coalesce;   /* 1 (default): write-backs booked by consecutive evict calls leave
+                               together at the next fence; 0: one K2 launch per evict call */
 } kvfh_sim_config;
 
 typedef struct {

@@ -15,7 +15,7 @@ class SimConfig(C.Structure):
         ("pcie_mode", C.c_uint32), ("pcie_ctas", C.c_uint32), ("numa_node", C.c_int32), ("audit", C.c_int32),
         ("verify_loads", C.c_int32), ("timing", C.c_int32), ("clock", C.c_int32), ("compute_scale", C.c_double),
         ("compute_ctas", C.c_uint32), ("prefetch_retry", C.c_int32), ("layered_gate", C.c_int32),
-        ("d2h_unbatched", C.c_int32),
+        ("d2h_unbatched", C.c_int32), ("d2h_coalesce", C.c_int32),
     ]
 
 

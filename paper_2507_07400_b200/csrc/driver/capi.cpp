@@ -117,6 +117,7 @@ void kvfh_default_config(kvfh_sim_config* c) {
     c->numa_node = -1;
     c->compute_scale = 1.0;
     c->compute_ctas = 128;
+    c->d2h_coalesce = 1;
 }
 
 int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
@@ -179,6 +180,7 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
         s->sim->wall.prefetch_retry = c->prefetch_retry != 0;
         s->sim->wall.layered_gate = c->layered_gate != 0;
         if (c->d2h_unbatched) s->sim->tier().set_offload_batching(false);
+        s->sim->tier().set_offload_coalescing(c->d2h_coalesce != 0 && !c->d2h_unbatched);
         // record every transition, tagged with the event index (same stream as ref_trace)
         auto prev = s->sim->tier().transition_observer;
         kvfh_sim* raw = s.get();

@@ -349,9 +349,13 @@ __global__ void __launch_bounds__(512) kvf_copy_vec_kernel(const __grid_constant
             if (threadIdx.x == 0) atomicAdd(p.layer_ready + plane / 2, 1u);
         }
     }
-    if (stamp) {
-        __syncthreads();  // (thread 0 only writes) every thread of the CTA is done
-        p.stamps[2 * blockIdx.x + 1] = gnow();
+    if (p.stamps && blockIdx.x < kvf_impl::kStampCtas) {
+        // a store to mapped host memory is posted: the CTA's last store instruction is not the
+        // bytes' arrival.  Every thread fences its own stores system-wide first, so the end
+        // stamp means "landed" for D2H as the stop event does (free for H2D: HBM stores)
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) p.stamps[2 * blockIdx.x + 1] = gnow();
     }
 }
 
