@@ -30,6 +30,6 @@ def test_reference_suite_on_the_gpu_engine(suite):
     r = subprocess.run([os.path.join(BIN, f"suite_{suite}")], capture_output=True, text=True, timeout=600)
     fails = {f"{os.path.basename(m.group(1))}:{m.group(2)}" for m in re.finditer(r"^FAIL (\S+):(\d+):", r.stdout, re.M)}
     expected = {k for k in KNOWN if k.startswith(f"test_{suite}.cpp")}
-    assert fails == expected, r.stdout[-3000:]
+    assert fails == expected, (r.returncode, r.stdout[-3000:], r.stderr[-3000:])
     m = re.search(r"test cases: (\d+) \| (\d+) passed", r.stdout)
     assert m and int(m.group(1)) - int(m.group(2)) == (3 if suite == "scheduler" else 0), r.stdout[-2000:]
