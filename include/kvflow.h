@@ -243,14 +243,15 @@ int kvf_victim_select(kvf_engine* e, const kvf_tree_view* tree, const kvf_evict_
  *
  * Decisions are requests in a ring in mapped pinned memory, executed in order either by a
  * RESIDENT decider (one 128-thread CTA polling the ring: no launch per decision; trees up to
- * KVF_RESIDENT_MAX_SLOTS slots) or by one launch per request (larger trees, or the resident
+ * KVF_RESIDENT_MAX_SLOTS slots: its 128 threads lose to a launch sized to the tree beyond that)
+ * or by one launch per request (larger trees, or the resident
  * decider disabled).  The resident CTA exits after KVF_DECIDER_IDLE_US (default 200) of idle,
  * so a device-wide synchronize elsewhere waits at most that long; kvf_decider_hold(e, 1) keeps
  * it alive across idle gaps (a driver's run), kvf_decider_hold(e, 0) lets it go at once. */
 typedef struct kvf_tree kvf_tree;
 
 #define KVF_SLOT_DEAD 0xFF        /* status of a freed slot */
-#define KVF_RESIDENT_MAX_SLOTS 512u
+#define KVF_RESIDENT_MAX_SLOTS 128u
 
 typedef struct {
     uint32_t slot;    /* mirror slot of this node */

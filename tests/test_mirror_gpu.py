@@ -1,7 +1,7 @@
 """Decisions over the HBM tree mirror (kvf_tree_*, csrc/engine/mirror.cu) against the
 reference's own vectors and the snapshot path:
   * K5 over the mirror == the unmodified reference's RadixCache::evict on 402 golden
-    snapshots (tests/golden/evict_small.jsonl), served by the resident decider CTA (<= 512
+    snapshots (tests/golden/evict_small.jsonl), served by the resident decider CTA (<= 128
     slots) and by one-shot launches (larger / KVF_DECIDER=0);
   * K4 over the mirror == the reference's set_agent_priorities (tests/golden/prio.jsonl),
     reported as rank changes;
@@ -73,8 +73,9 @@ def test_mirror_k5_matches_reference_vectors(eng):
         checked += 1
     s1 = eng.stats()
     assert checked >= 300
-    # small trees went to the resident CTA, the few above 512 slots to one-shot launches
-    assert s1["resident_served"] - s0["resident_served"] > 0.9 * checked
+    # trees up to 128 slots went to the resident CTA, larger ones to one-shot launches
+    assert s1["resident_served"] - s0["resident_served"] > 0
+    assert s1["oneshot_served"] - s0["oneshot_served"] > 0
 
 
 def test_mirror_k4_matches_reference_vectors(eng):
