@@ -73,9 +73,9 @@ def test_mirror_k5_matches_reference_vectors(eng):
         checked += 1
     s1 = eng.stats()
     assert checked >= 300
-    # trees up to 128 slots went to the resident CTA, larger ones to one-shot launches
-    assert s1["resident_served"] - s0["resident_served"] > 0
-    assert s1["oneshot_served"] - s0["oneshot_served"] > 0
+    # these trees (<= 128 slots) went to the resident CTA; larger ones (the incremental test
+    # below grows to 900 slots) take one-shot launches
+    assert s1["resident_served"] - s0["resident_served"] >= checked
 
 
 def test_mirror_k4_matches_reference_vectors(eng):
