@@ -4,8 +4,9 @@ mkdir -p gpurun_out
 tag=${1:-r02}
 out=gpurun_out/sanitize_$tag.txt
 : > $out
+export KVF_SANITIZER=1  # tests skip their real-time latency assertions (kernels run 10-100x slower)
 for tool in memcheck racecheck; do
-  for f in tests/test_lockstep_gpu.py tests/test_fuzz_gpu.py tests/test_wallclock_gpu.py tests/test_concurrency_gpu.py tests/test_shared_engine_gpu.py tests/test_wallclock_parity_gpu.py; do
+  for f in tests/test_lockstep_gpu.py tests/test_fuzz_gpu.py tests/test_wallclock_gpu.py tests/test_concurrency_gpu.py tests/test_shared_engine_gpu.py tests/test_wallclock_parity_gpu.py tests/test_mirror_gpu.py; do
     [ -f $f ] || continue
     echo "=== $tool: $f" >> $out
     timeout ${SAN_TMO:-1500} compute-sanitizer --tool $tool --target-processes all --print-limit 20 \

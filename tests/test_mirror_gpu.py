@@ -20,6 +20,7 @@ import time
 import numpy as np
 import pytest
 
+from conftest import UNDER_SANITIZER
 from oracle_ffi import ORACLE_DIR, TreeArrays, load_jsonl
 
 pytestmark = pytest.mark.gpu
@@ -300,4 +301,5 @@ def test_resident_fast_path_latency(eng):
             decider_hold(eng, False)
     med = sorted(lat)[len(lat) // 2]
     print(f"K4+K5 pair via the resident decider, {len(a['parent'])} nodes: median {med:.1f} us")
-    assert med < 60
+    if not UNDER_SANITIZER:
+        assert med < 60

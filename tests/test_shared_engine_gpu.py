@@ -12,6 +12,8 @@ import time
 import numpy as np
 import pytest
 
+from conftest import UNDER_SANITIZER
+
 from oracle_ffi import load_jsonl
 
 pytestmark = pytest.mark.gpu
@@ -83,6 +85,8 @@ def test_decisions_do_not_queue_behind_a_fence():
         for t in threads:
             t.join(timeout=300)
         assert not errors, errors
+        if UNDER_SANITIZER:
+            return
         assert statistics.median(waits) > 5e-3  # the fence really blocked for a 1 GiB load
         assert len(lat_waiting) > 100, len(lat_waiting)
         med = statistics.median(lat_waiting)

@@ -11,6 +11,8 @@ import sys
 
 import pytest
 
+from conftest import UNDER_SANITIZER
+
 pytestmark = pytest.mark.gpu
 pytest.importorskip("paper_2507_07400_b200.sim")
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
@@ -24,6 +26,8 @@ def test_wall_clock_decisions_equal_reference(cfg):
     assert run["node_transitions_equal"], run["nodes_differing"]
     b = run["bytes_verified"]
     assert b["load_failures"] == 0 and b["resident_bad"] == 0 and b["loads"] > 0
+    if UNDER_SANITIZER:
+        return
     # the steps the reference served by prefetch start within host decision latency (no PCIe wait)
     st = run["prefetch_served_stall_us"]
     assert run["prefetch_served_steps"] == 37
