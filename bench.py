@@ -218,6 +218,19 @@ def run_ours(args, rank, world, local):
     # parity spot check of the bench's own bytes (device copy == host source)
     ok = eng.checksum(N.KVF_TIER_DEVICE, dev_fixed[(args.warmup + args.steps - 1) % 2]) == \
         eng.checksum(N.KVF_TIER_HOST, fixed_host[(args.warmup + args.steps) % 4])
+    # K1 comparators over the same node and runs: the copy engine, one cudaMemcpy2DAsync per
+    # piece vs every (piece, plane) segment in one cudaMemcpyBatchAsync
+    comparators = {}
+    for name, mode in (("ce_memcpy2d", N.KVF_COPY_CE), ("ce_memcpy_batch", N.KVF_COPY_CE_BATCH)):
+        eng.set_copy_mode(mode)
+        ts = []
+        for rep in range(3):
+            j = eng.h2d(fixed_host[rep % 4], dev_fixed[rep % 2])
+            ts.append(eng.elapsed_ms(j))
+            eng.release(j)
+        comparators[name] = round(pre_bytes / (min(ts) * 1e-3) / 1e9, 3)
+    eng.set_copy_mode(N.KVF_COPY_SM_VEC)
+    comparators["sm_vec_k1"] = round(pre_bytes / (min(k1_ms) * 1e-3) / 1e9, 3)
     # K3 on-device gather of one 1 GiB/N node (HBM roofline)
     stage = torch.empty(pre_bytes, dtype=torch.uint8, device=f"cuda:{local}")
     k3 = []
@@ -271,7 +284,7 @@ def run_ours(args, rank, world, local):
     total_step_ms = sum(step_ms)
     mine = {
         "step_ms": total_step_ms, "wall": wall, "e2e_wall": e2e_wall, "k1_avg_ms": statistics.mean(k1_ms),
-        "k3_ms": min(k3), "k2_avg_ms": statistics.mean(k2_ms), "parity_ok": ok,
+        "k3_ms": min(k3), "k2_avg_ms": statistics.mean(k2_ms), "parity_ok": ok, "comparators": comparators,
     }
     if world > 1:
         t = torch.tensor([total_step_ms, wall, e2e_wall, mine["k1_avg_ms"], float(not ok)], dtype=torch.float64,
@@ -338,6 +351,7 @@ def run_ours(args, rank, world, local):
             "us_per_layer_call_single": round(k6["ms_single"] * 1e3, 2),
             "workload": "rank 0: 2 sequences x 8320 tokens (prefetched node + suffix), group 4, 32 layers"},
         "pcie_peaks_gbs": {k: round(v, 3) for k, v in pcie.items()},
+        "k1_comparators_gbs": mine.get("comparators"),
         # the reference's own figure for this transfer is its cost model: 64e9 * 0.6 B/s + 50 us
         # per job (proj/src/cost_model.cpp:47-50) -> 38.33 GB/s for a 1 GiB node
         "vs_reference_cost_model": round(value / world / ((1 << 30) / ((1 << 30) / (64e9 * 0.6) + 50e-6) / 1e9), 3),
