@@ -151,7 +151,6 @@ struct DeciderState {
     bool disabled = false;   // KVF_DECIDER=0: one launch per request
     bool res_attr_set = false, once_attr_set = false;
     uint64_t epoch = 0;      // launch count of the resident CTA (its exit word carries it)
-    uint64_t res_first = 0;  // first request the running resident CTA serves
     uint64_t last_res_post = 0;  // last request handed to the resident CTA
     uint64_t idle_ns = 200000;
     uint32_t res_cap = 0;    // slots the resident CTA's shared memory is sized for

@@ -280,15 +280,11 @@ __device__ __forceinline__ void serve(const ReqSlot& slot, Ctl* ctl, unsigned lo
 // host wrote the slot before the launch, so the first read normally holds it.
 __global__ void __launch_bounds__(kThreads) kvf_decide_once(const ReqSlot* slot, Ctl* ctl, unsigned long long seq) {
     __shared__ ReqSlot req;
-    __shared__ int s_ok;
     __shared__ unsigned long long s_polls;
     if (threadIdx.x < 32) {
         unsigned long long polls = 1;
         while (!read_slot(req, slot, seq, nullptr, nullptr)) ++polls;
-        if (threadIdx.x == 0) {
-            s_ok = 1;
-            s_polls = polls;
-        }
+        if (threadIdx.x == 0) s_polls = polls;
     }
     __syncthreads();
     serve(req, ctl, seq, s_polls);
@@ -430,7 +426,6 @@ int launch_resident(kvf_engine* e, uint64_t first) {
         d.hold ? ~0ull : d.idle_ns);
     KVF_CUDA(cudaGetLastError());
     d.running = true;
-    d.res_first = first;
     e->stats.kernel_launches++;
     e->stats.resident_launches++;
     return KVF_OK;
