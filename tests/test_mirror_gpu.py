@@ -303,3 +303,44 @@ def test_resident_fast_path_latency(eng):
     print(f"K4+K5 pair via the resident decider, {len(a['parent'])} nodes: median {med:.1f} us")
     if not UNDER_SANITIZER:
         assert med < 60
+
+
+def test_mirror_grows_past_its_capacity_with_a_k4_pending(eng):
+    """A tree that outgrows its mirror (1024 -> 6000 slots: a new HBM block, the old slots
+    copied, the single-CTA path handing over to the device-wide one) while a queued K4's result
+    is still unread: the rank changes survive the move and K4 / K5 agree with the snapshot
+    forms on the grown tree."""
+    from paper_2507_07400_b200.engine import Tree
+    rng = np.random.default_rng(9)
+    n = 6000
+    parent = np.zeros(n, dtype=np.int32)
+    parent[0] = -1
+    for i in range(1, n):
+        parent[i] = rng.integers(0, i)
+    suffix = 4611686018427387903
+    recs = [{"slot": i, "parent": int(parent[i]), "lock": 1 if i == 0 else 0, "status": 0, "backed": 0,
+             "rank": suffix, "time": float(i), "seq": i, "id": i, "tokens": int(rng.integers(1, 9))} for i in range(n)]
+    with Tree(eng, 5) as t:
+        t.update(recs[:800])
+        bs = [int(x) for x in rng.integers(1, 800, size=6)]
+        cands = [1, 2, 3, 4, 5, 6]
+        t.priorities(bs, cands)            # queued on the 1024-slot mirror ...
+        t.update(recs[800:])               # ... the next request needs 6000 slots
+        t.hints(True)
+        slots, acts, imm, pend = t.victims(needed=400, workflow_aware=True, offload=True)
+        ch = t.rank_changes()              # the K4 result, carried across the move
+        want = eng.priority(parent[:800], bs, cands)
+        got = [ch.get(i, suffix) for i in range(1, 800)]
+        assert got == [int(x) for x in want[1:]]
+        # the K5 above ran before the K4's ranks reached the host, on the grown mirror with them
+        ranks = np.full(n, suffix, dtype=np.int64)
+        ranks[:800] = want
+        ranks[0] = suffix
+        tree = dict(parent=parent, status=np.zeros(n, np.uint8), lock=(np.arange(n) == 0).astype(np.int32),
+                    rank=ranks, time=np.arange(n, dtype=np.float64), seq=np.arange(n, dtype=np.uint64),
+                    id=np.arange(n, dtype=np.uint64), tokens=np.array([r["tokens"] for r in recs], np.uint64),
+                    backed=np.zeros(n, np.uint8), bpt=5)
+        from paper_2507_07400_b200.engine import depth_from_parent
+        tree["depth"] = depth_from_parent(parent)
+        wi, wa, wimm, wpend = eng.victims(tree, 400, True, True)
+        assert slots.tolist() == wi.tolist() and acts.tolist() == wa.tolist() and (imm, pend) == (wimm, wpend)
