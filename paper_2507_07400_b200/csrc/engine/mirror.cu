@@ -830,8 +830,10 @@ int kvf_tree_update(kvf_tree* t, const kvf_node_rec* recs, uint32_t n) {
     for (uint32_t i = 0; i < n; ++i) {
         const kvf_node_rec& r = recs[i];
         if (r.slot >= (1u << 24)) return set_error(KVF_E_INVALID_ARG, "slot beyond 2^24");
-        if (r.parent >= static_cast<int32_t>(1u << 24)) return set_error(KVF_E_INVALID_ARG, "parent slot beyond 2^24");
-        t->n = std::max<uint32_t>(t->n, r.slot + 1);
+        if (r.parent >= static_cast<int32_t>(1u << 24) || r.parent < -1)
+            return set_error(KVF_E_INVALID_ARG, "parent slot outside [-1, 2^24)");
+        // a parent named before its own record arrives still lies inside the mirror
+        t->n = std::max<uint32_t>(t->n, std::max<uint32_t>(r.slot + 1, static_cast<uint32_t>(r.parent + 1)));
         t->keys.note(r);
     }
     t->staged.insert(t->staged.end(), recs, recs + n);
