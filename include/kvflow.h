@@ -73,9 +73,7 @@ enum { KVF_TIER_DEVICE = 0, KVF_TIER_HOST = 1 };
 enum {
     KVF_COPY_SM_VEC = 0,  /* LDG.128 / STG.128 SM-driven zero-copy (host pool is mapped pinned) */
     KVF_COPY_SM_BULK = 1, /* cp.async.bulk (TMA bulk engine) staging through shared memory      */
-    KVF_COPY_CE = 2,      /* copy engine (cudaMemcpy2DAsync per piece) -- comparator only      */
-    KVF_COPY_CE_BATCH = 3 /* copy engine, every (piece, plane) segment of a job in ONE
-                             cudaMemcpyBatchAsync -- comparator only            */
+    KVF_COPY_CE = 2       /* copy engine (cudaMemcpy2DAsync per piece) -- comparator only      */
 };
 
 typedef struct kvf_engine kvf_engine; /* opaque */

@@ -20,7 +20,7 @@ DRIVER_SO = os.path.join(PKG, "libkvflow_driver.so")
 
 KVF_OK = 0
 KVF_TIER_DEVICE, KVF_TIER_HOST = 0, 1
-KVF_COPY_SM_VEC, KVF_COPY_SM_BULK, KVF_COPY_CE, KVF_COPY_CE_BATCH = 0, 1, 2, 3
+KVF_COPY_SM_VEC, KVF_COPY_SM_BULK, KVF_COPY_CE = 0, 1, 2
 KVF_NUMA_AUTO = -2
 KVF_E_INVALID_ARG, KVF_E_OUT_OF_HOST_SLOTS, KVF_E_NO_DEVICE, KVF_E_UNKNOWN_JOB, KVF_E_TOO_LARGE = 101, 102, 103, 104, 105
 

@@ -515,7 +515,11 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
     }
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
     const uint32_t hkv = e->geom.kv_heads_local, hq = hkv * group;
-    const uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta));  // heads per CTA
+    uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta));  // heads per CTA
+    if (const char* f = std::getenv("KVF_ATTEND_HPC")) {  // sweep knob (scripts/attend_hpc_sweep.py)
+        const uint32_t want = static_cast<uint32_t>(std::atoi(f));
+        if (want && hpc % want == 0) hpc = want;
+    }
     const uint32_t ygrid = hkv / hpc;
     if (ygrid > 65535 || batch >= (1u << 31) || hq > 65535)
         return set_error(KVF_E_TOO_LARGE, "batch or head count too large");
@@ -529,6 +533,7 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
     sig.push_back(batch);
     sig.push_back(group);
     sig.push_back(chunk_tokens);
+    sig.push_back(hpc);
     for (uint32_t b = 0; b < batch; ++b) sig.push_back(run_counts[b]);
     for (uint64_t k = 0; k < nruns; ++k) {
         sig.push_back(runs[k].start);

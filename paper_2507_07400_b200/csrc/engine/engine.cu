@@ -581,27 +581,6 @@ int launch_copy(kvf_engine* e, cudaStream_t stream, const Endpoint& src, const E
             }
             continue;
         }
-        if (mode == KVF_COPY_CE_BATCH) {  // every (piece, plane) segment in ONE cudaMemcpyBatchAsync
-            std::vector<void*> dsts, srcs;
-            std::vector<size_t> sizes;
-            dsts.reserve(static_cast<size_t>(np) * planes);
-            srcs.reserve(dsts.capacity());
-            sizes.reserve(dsts.capacity());
-            for (uint32_t i = 0; i < np; ++i) {
-                const Piece& pc = pieces[first + i];
-                for (uint32_t pl = 0; pl < planes; ++pl) {
-                    dsts.push_back(const_cast<char*>(dst.base) + pl * dst.stride + pc.dst_slot * tpb);
-                    srcs.push_back(const_cast<char*>(src.base) + pl * src.stride + pc.src_slot * tpb);
-                    sizes.push_back(pc.ntok * tpb);
-                }
-            }
-            cudaMemcpyAttributes attr{};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            size_t aidx = 0, fail = 0;
-            KVF_CUDA(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &aidx, 1, &fail,
-                                          stream));
-            continue;
-        }
         CopyParams p;
         std::memset(&p, 0, sizeof(p));
         p.src = src.base;
@@ -983,7 +962,7 @@ int kvf_engine_set_job_timing(kvf_engine* e, uint32_t mode) {
 
 int kvf_engine_set_copy_mode(kvf_engine* e, uint32_t mode, uint32_t pcie_ctas, uint32_t hbm_ctas) {
     KVF_GUARD(e);
-    if (mode > KVF_COPY_CE_BATCH) return set_error(KVF_E_INVALID_ARG, "unknown copy mode");
+    if (mode > KVF_COPY_CE) return set_error(KVF_E_INVALID_ARG, "unknown copy mode");
     e->cfg.pcie_mode = mode;
     if (pcie_ctas) e->cfg.pcie_ctas = pcie_ctas;
     if (hbm_ctas) e->cfg.hbm_ctas = hbm_ctas;

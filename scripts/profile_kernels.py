@@ -57,6 +57,29 @@ def main(which):
             e.victims(tree, c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"], c["cpu_used"],
                       c["cpu_cap"])
         print("k5 nodes", ta.n)
+    if which in ("k5mirror", "k5big"):
+        # K5 over the HBM mirror: a 1.4k-node golden tree (one-shot kvf_decide_once; run with
+        # KVF_DECIDER=0 so no resident CTA is in the capture) or a 30k-node tree on the
+        # hand-written device-wide path (big_* kernels)
+        import subprocess
+        from oracle_ffi import ORACLE_DIR, TreeArrays, load_jsonl
+        from paper_2507_07400_b200.engine import Tree
+        if which == "k5mirror":
+            c = sorted(load_jsonl("evict_medium.jsonl"), key=lambda c: -len(c["parent"]))[0]
+        else:
+            import json
+            out = subprocess.run([os.path.join(ORACLE_DIR, "_ref", "ref_trace"), "evict", "seed=7", "cases=1",
+                                  "min_nodes=30000", "max_nodes=30000", "vocab=200"], capture_output=True, text=True,
+                                 check=True).stdout
+            c = json.loads(out.splitlines()[0])
+        ta = TreeArrays(c)
+        arr = {k: getattr(ta, k) for k in ("parent", "status", "lock", "rank", "time", "seq", "id", "tokens", "backed")}
+        with Tree(e, ta.bpt, capacity=ta.n) as t:
+            t.load_arrays(arr)
+            t.hints(True)
+            for _ in range(6):
+                t.victims(c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"], c["cpu_used"], c["cpu_cap"])
+        print(which, "nodes", ta.n)
     e.close()
 
 

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 N = pytest.importorskip("paper_2507_07400_b200._native")
 from paper_2507_07400_b200.engine import Engine, depth_from_parent  # noqa: E402
 
-MODES = [N.KVF_COPY_SM_VEC, N.KVF_COPY_SM_BULK, N.KVF_COPY_CE, N.KVF_COPY_CE_BATCH]
+MODES = [N.KVF_COPY_SM_VEC, N.KVF_COPY_SM_BULK, N.KVF_COPY_CE]
 
 
 def oracle_geom(e):
