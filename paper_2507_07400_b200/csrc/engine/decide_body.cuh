@@ -562,6 +562,7 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         o.header[2] = s_pend;
     }
     stamp(5);
+    __syncthreads();  // thread 0's last stamps before warp 0 copies them out
     if (threadIdx.x < 12) o.header[threadIdx.x < 6 ? 3 + threadIdx.x : 9 + (threadIdx.x - 6)] = s_stamp[threadIdx.x];
     if (o.spin) publish_done(o.header + kDoneWord, seq);  // else the caller publishes (mirror.cu)
 }
