@@ -90,11 +90,6 @@ struct AttnParams {
     float* part_o;             // [items][hkv][group][128]
     float* part_ml;            // [items][hkv][group][2]
     unsigned long long* trace; // diagnostics (KVF_ATTEND_TRACE): per CTA start, prologue, loop, end, smid
-    // fold: the split-KV combine runs in this kernel -- the last CTA of each (sequence, head
-    // group) to finish merges the group's partials (counters self-reset for the next call)
-    const uint32_t* seq_item0; // first item of each sequence (items of a sequence are contiguous)
-    uint32_t* counters;        // [batch][gridDim.y] finished items
-    uint32_t fold;
     uint32_t inline_items;     // 1: items[] below (grid <= kParamItems), else p.items in global memory
     AttnItem items_p[kParamItems];
 };
@@ -139,54 +134,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 // byte offset of 16-B chunk c of row r inside a [16 rows][256 B] tile (XOR swizzle, low 3 bits)
 __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t c) { return r * kRowBytes + ((c ^ (r & 7)) << 4); }
-
-// The split-KV combine inside the main kernel.  Every CTA of a multi-item sequence publishes
-// its partials, then counts itself done for its (sequence, head group); the LAST one merges
-// the group's partials of all the sequence's items -- out = sum_i 2^(m_i - M) o_i / sum_i
-// 2^(m_i - M) l_i -- and resets the counter.  With 1-2 heads per CTA that is a few tens of
-// KB of L2-resident partials, read by 256 threads in two independent-load passes (maxima,
-// then the weighted sums), instead of a second kernel and its launch.
-__device__ __noinline__ void fold_merge(const AttnParams& p, const AttnItem& it, uint32_t tid) {
-    __shared__ uint32_t s_last;
-    __threadfence();  // this CTA's partials before its count
-    __syncthreads();
-    uint32_t* ctr = p.counters + static_cast<uint64_t>(it.seq) * gridDim.y + blockIdx.y;
-    if (tid == 0) s_last = atomicAdd(ctr, 1u) == it.nsib - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();  // every other CTA's partials are visible past its count
-    const uint32_t i0 = p.seq_item0[it.seq], n = it.nsib;
-    // outputs of the group: hpc heads x group rows x 32 float4 of the 128 dims
-    const uint32_t nout = p.hpc * p.group * (kD / 4);
-    for (uint32_t e = tid; e < nout; e += kThreads) {
-        const uint32_t hl = e / (p.group * (kD / 4)), row = (e / (kD / 4)) % p.group, c4 = e % (kD / 4);
-        const uint32_t head = blockIdx.y * p.hpc + hl;
-        auto key = [&](uint32_t i) { return (static_cast<uint64_t>(i0 + i) * p.hkv + head) * p.group + row; };
-        float M = -INFINITY;
-#pragma unroll 8
-        for (uint32_t i = 0; i < n; ++i) M = fmaxf(M, p.part_ml[key(i) * 2]);
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        float l = 0.f;
-#pragma unroll 4
-        for (uint32_t i = 0; i < n; ++i) {
-            const uint64_t k = key(i);
-            const float2 ml = *reinterpret_cast<const float2*>(p.part_ml + k * 2);
-            const float sc = ml.x == -INFINITY ? 0.f : exp2f(ml.x - M);
-            const float4 v = reinterpret_cast<const float4*>(p.part_o + k * kD)[c4];
-            o.x += sc * v.x;
-            o.y += sc * v.y;
-            o.z += sc * v.z;
-            o.w += sc * v.w;
-            l += sc * ml.y;
-        }
-        const float r = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(
-            p.out + ((static_cast<uint64_t>(it.seq) * p.hq + head * p.group + row) * kD + c4 * 4));
-        ob[0] = __floats2bfloat162_rn(o.x * r, o.y * r);
-        ob[1] = __floats2bfloat162_rn(o.z * r, o.w * r);
-    }
-    if (tid == 0) *ctr = 0;  // the next call (or layer) counts from zero again
-}
 
 __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_constant__ AttnParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -381,7 +328,6 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
                 p.part_ml[(pk + row) * 2 + 1] = l;
             }
         }
-        if (p.fold && it.nsib > 1) fold_merge(p, it, tid);
         if (p.trace) {
             __syncthreads();
             if (tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
@@ -444,7 +390,6 @@ __global__ void __launch_bounds__(kThreads, 1) kvf_attend_kernel(const __grid_co
             }
         }
     }
-    if (p.fold && it.nsib > 1) fold_merge(p, it, tid);
     if (p.trace) {
         __syncthreads();
         if (tid == 0) p.trace[(static_cast<uint64_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 5 + 3] = gtime();
@@ -570,15 +515,13 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
     }
     if (e->jobs.count(job_id)) return set_error(KVF_E_INVALID_ARG, "job id " + std::to_string(job_id) + " already in use");
     const uint32_t hkv = e->geom.kv_heads_local, hq = hkv * group;
-    // split-KV combine folded into the main kernel (fold_merge) unless KVF_ATTEND_FOLD=0; its
-    // merge reads hpc heads' partials, so folding takes 2 heads per CTA (same loop rate as 8,
-    // scripts/attend_hpc_sweep.py) instead of all the shard's heads
-    static const bool fold = [] {
-        const char* f = std::getenv("KVF_ATTEND_FOLD");
-        return !(f && f[0] == '0');
-    }();
-    uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(fold ? 2 : kMaxHeadsCta));  // heads per CTA
-    if (const char* f = std::getenv("KVF_ATTEND_HPC")) {  // sweep knob (scripts/attend_hpc_sweep.py)
+    // KV heads per CTA.  A single-layer call takes 2 (more, shorter items per sequence: the
+    // wave ends more evenly -- C2 2 x 8320 23.0 -> 21.2 us, C4 64 x 1792 88.7 -> 78.3 us per call);
+    // a PDL-chained step keeps all of the shard's heads (dense 2 KiB token rows; the chain
+    // already hides the wave's end: C2 13.1 us per layer vs 13.6 with 2).
+    // scripts/attend_hpc_sweep.py, profiles/r02_attend_hpc_sweep.json
+    uint32_t hpc = std::gcd(hkv, static_cast<uint32_t>(nlayers == 1 ? 2 : kMaxHeadsCta));
+    if (const char* f = std::getenv("KVF_ATTEND_HPC")) {  // sweep knob
         const uint32_t want = static_cast<uint32_t>(std::atoi(f));
         if (want && std::gcd(hkv, static_cast<uint32_t>(kMaxHeadsCta)) % want == 0) hpc = want;
     }
@@ -699,9 +642,8 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
                      b_si = al((batch + 1) * 4), b_em = al(empty.size() * 4);
         const size_t b_po = multi ? al(nitems * hkv * group * kD * 4) : 0;
         const size_t b_pm = multi ? al(nitems * hkv * group * 2 * 4) : 0;
-        const size_t b_ct = al(static_cast<size_t>(batch) * ygrid * 4);  // fold counters
         const size_t in_bytes = b_items + b_rt + b_rs + b_si + b_em;
-        const size_t dev_need = in_bytes + b_po + b_pm + b_ct;
+        const size_t dev_need = in_bytes + b_po + b_pm;
         // grow the workspace only between calls: cudaFree must not race an in-flight reader
         if (dev_need > e->ws_att.dev_bytes || in_bytes > e->ws_att.host_bytes) {
             KVF_CUDA(cudaStreamSynchronize(e->s_cmp));
@@ -722,14 +664,11 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
         int rc = begin_job(e, job_id, e->s_cmp, j);
         if (rc) return rc;
         KVF_CUDA(cudaMemcpyAsync(e->ws_att.dev, hs, in_bytes, cudaMemcpyHostToDevice, e->s_cmp));
-        // fold counters start at zero; every call leaves them at zero again
-        KVF_CUDA(cudaMemsetAsync(static_cast<char*>(e->ws_att.dev) + in_bytes + b_po + b_pm, 0,
-                                 static_cast<size_t>(batch) * ygrid * 4, e->s_cmp));
         KVF_CUDA(cudaEventRecord(e->att_upload_done, e->s_cmp));
         e->att_upload_pending = true;
         e->att_sig.swap(sig);
-        const uint64_t m[11] = {nitems, total_tok, in_bytes, b_items, b_rt, b_rs, b_si, b_po, empty.size(), multi, b_pm};
-        std::copy(m, m + 11, meta);
+        const uint64_t m[10] = {nitems, total_tok, in_bytes, b_items, b_rt, b_rs, b_si, b_po, empty.size(), multi};
+        std::copy(m, m + 10, meta);
     } else {
         int rc = begin_job(e, job_id, e->s_cmp, j);
         if (rc) return rc;
@@ -737,7 +676,7 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
     // KV written by fills / K3 scatters on the dev stream must be visible to the reads
     if (e->dev_write_pending) KVF_CUDA(cudaStreamWaitEvent(e->s_cmp, e->dev_write_done, 0));
     const uint64_t nitems = meta[0], total_tok = meta[1], in_bytes = meta[2], b_items = meta[3], b_rt = meta[4],
-                   b_rs = meta[5], b_si = meta[6], b_po = meta[7], nempty = meta[8], multi = meta[9], b_pm = meta[10];
+                   b_rs = meta[5], b_si = meta[6], b_po = meta[7], nempty = meta[8], multi = meta[9];
     char* ds = static_cast<char*>(e->ws_att.dev);
 
     AttnParams prm{};
@@ -760,9 +699,6 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
     const uint32_t* d_empty = reinterpret_cast<const uint32_t*>(ds + b_items + b_rt + b_rs + b_si);
     prm.part_o = reinterpret_cast<float*>(ds + in_bytes);
     prm.part_ml = reinterpret_cast<float*>(ds + in_bytes + b_po);
-    prm.seq_item0 = d_seq_item0;
-    prm.counters = reinterpret_cast<uint32_t*>(ds + in_bytes + b_po + b_pm);
-    prm.fold = fold ? 1 : 0;
     if (!e->attend_attr_set) {
         KVF_CUDA(cudaFuncSetAttribute(kvf_attend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(kSmemBytes)));
@@ -794,7 +730,7 @@ int attend_impl(kvf_engine* e, uint64_t job_id, uint32_t layer0, uint32_t nlayer
             KVF_CUDA(cudaLaunchKernelEx(&cfg, kvf_attend_kernel, prm));
             e->stats.kernel_launches++;
         }
-        if (multi && !fold) {
+        if (multi) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(batch, hq);
             cfg.blockDim = dim3(kCombWarps * 32);

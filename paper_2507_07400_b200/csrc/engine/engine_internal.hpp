@@ -202,7 +202,7 @@ struct kvf_engine {
     int attend_occ = 0;  // resident K6 CTAs per SM
     std::vector<uint64_t> att_sig;  // K6 descriptor cache: inputs of the blob now in ws_att.dev
     std::vector<uint8_t> att_items;  // K6 work items of that blob (host copy for the launch parameters)
-    uint64_t att_meta[11] = {};     //   and its sizes (a decode step calls K6 once per layer)
+    uint64_t att_meta[10] = {};     //   and its sizes (a decode step calls K6 once per layer)
     kvf_impl::Workspace ws_big;  // snapshot upload for the device-wide K5 (grown on demand)
     kvf_impl::LargeState large_snap;  // device-wide K5 state of kvf_victim_select
 

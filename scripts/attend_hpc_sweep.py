@@ -14,7 +14,7 @@ r = A.run(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), [int(x) for x in sys.
 print(json.dumps({k: r[k] for k in ("layer_call_ms_median", "frac", "chained_layer_us", "chained_frac")}))
 ''' % (ROOT, ROOT)
 rows = []
-folds = sys.argv[1:] or ["1", "0"]
+folds = sys.argv[1:] or ["0"]  # KVF_ATTEND_FOLD: the folded combine was measured and removed
 for name, kv, g, lens, layers, hpcs in (("C2 2x8320", 8, 4, "8320,8320", 32, (8, 2, 1)),
                                         ("C2 4x8320", 8, 4, "8320,8320,8320,8320", 32, (8, 2, 1)),
                                         ("C4 64x1792", 8, 4, ",".join(["1792"] * 64), 32, (8, 2)),
