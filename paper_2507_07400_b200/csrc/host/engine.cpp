@@ -68,11 +68,13 @@ Engine::Engine(const EngineOptions& opt) : opt_(opt) {
 Engine::~Engine() { kvf_engine_destroy(e_); }
 
 RunList Engine::alloc(int tier, uint64_t tokens) {
-    RunList out(std::max<uint64_t>(1, std::min<uint64_t>(tokens, 4096)));
+    // the allocator keeps runs long (best fit, else largest first): a handful of entries is
+    // the common case -- a 4096-entry buffer zeroed per call cost ~3 us on every load / insert
+    RunList out(static_cast<size_t>(std::max<uint64_t>(1, std::min<uint64_t>(tokens, 16))));
     uint32_t n = 0;
     int rc = kvf_slots_alloc(e_, tier, tokens, out.data(), static_cast<uint32_t>(out.size()), &n);
-    if (rc == KVF_E_TOO_LARGE) {  // heavily fragmented pool: retry with room for every run
-        out.resize(1u << 20);
+    for (size_t cap = 4096; rc == KVF_E_TOO_LARGE && out.size() < (1u << 20); cap = 1u << 20) {
+        out.resize(std::min<uint64_t>(std::max<uint64_t>(tokens, 1), cap));  // fragmented pool: room for more runs
         rc = kvf_slots_alloc(e_, tier, tokens, out.data(), static_cast<uint32_t>(out.size()), &n);
     }
     if (rc != KVF_OK) throw_engine(rc, "kvf_slots_alloc");

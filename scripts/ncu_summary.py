@@ -26,11 +26,27 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "Kernel Name"]
 
 
-def raw(rep):
+def raw(rep, row=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, units, vals = rows[0], rows[1], rows[2]
+    h, units, vals = rows[0], rows[1], rows[2 + row]
     return {w: (units[h.index(w)], vals[h.index(w)]) for w in WANT if w in h}
+
+
+def all_rows(rep):
+    """Every kernel of a multi-kernel capture (the device-wide K5 graph): name, duration, grid."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        if len(vals) < len(h):
+            continue
+        u = units[h.index("gpu__time_duration.sum")]
+        res.append({"kernel": vals[h.index("Kernel Name")],
+                    "duration_us": float(vals[h.index("gpu__time_duration.sum")].replace(",", "")) * UNIT.get(u, 1.0) * 1e6,
+                    "grid": vals[h.index("launch__grid_size")], "block": vals[h.index("launch__block_size")]})
+    return res
 
 
 def scaled(m, key):
@@ -73,16 +89,28 @@ def shares(path):
     return {k: {"launches": n, "share": round(t / tot, 4)} for k, (n, t) in sorted(per.items(), key=lambda x: -x[1][1])}
 
 
-def main(tag):
-    out = {"tag": tag}
-    for k in ("k1", "k2", "k3", "k5", "k6"):
+def main(tag, dst_name="ncu_summary.json"):
+    dst = os.path.join(ROOT, "profiles", dst_name)
+    # kernels not re-captured under this tag keep their earlier summaries (marked with theirs)
+    out = json.load(open(dst)) if os.path.exists(dst) else {}
+    prev = out.get("tag")
+    for k, v in list(out.items()):
+        if isinstance(v, dict) and "kernel" in v and "tag" not in v:
+            v["tag"] = prev
+    out["tag"] = tag
+    for k in ("k1", "k2", "k3", "k5", "k6", "k5m"):
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{k}_{tag}.ncu-rep")
         if os.path.exists(rep):
             out[k] = kernel(rep, k)
+            out[k]["tag"] = tag
+    rep = os.path.join(ROOT, "gpurun_out", f"prof_k5big_{tag}.ncu-rep")
+    if os.path.exists(rep):
+        ks = all_rows(rep)
+        out["k5_device_wide"] = {"tag": tag, "what": "hand-written device-wide K5 kernels of one 30k-node call",
+                                 "kernels": ks, "total_us": round(sum(k["duration_us"] for k in ks), 2)}
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lp):
         out["launch_shares_bench"] = shares(lp)
-    dst = os.path.join(ROOT, "profiles", "ncu_summary.json")
     with open(dst, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))
