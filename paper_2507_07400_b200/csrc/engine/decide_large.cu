@@ -320,6 +320,8 @@ __global__ void __launch_bounds__(kThr) big_tile_scan(Pair* tsum, uint32_t tiles
 __global__ void __launch_bounds__(kThr) big_emit(LargeArrays a, const BigReq* q, const uint32_t* vals,
                                                  const uint8_t* flags, const int32_t* eff, Hdr* hdr, const Pair* tsum,
                                                  uint32_t* out_idx, uint8_t* out_act) {
+    // a tile whose bytes-before already reach `needed` pops nothing: skip its chain walks
+    if (tsum[blockIdx.x].b >= q->needed) return;  // uniform per CTA
     const uint32_t c = static_cast<uint32_t>(hdr->cands);
     const uint32_t k0 = blockIdx.x * kTile + threadIdx.x * (kTile / kThr);
     Pair per[kTile / kThr];
