@@ -13,11 +13,12 @@
 //        eff(n)      = max(ord(n), eff(device children))   ord = position in `before` order
 //        victims     = R sorted by (eff asc, depth desc), cut at the first prefix whose
 //                      byte sum reaches `needed`.
-//     One CTA, everything in shared memory: a bitonic sort of the candidates by the
-//     4-word key, R and eff by parallel root walks (shared-memory atomics with early
-//     exit, no per-level barriers), a bitonic sort of 64-bit (eff, depth, idx) keys, and
-//     a block scan for the byte cut.  Both sorts hold one to four elements per thread in
-//     registers (bitonic_reg): only the stages spanning more than a warp touch shared memory.
+//     One CTA, everything in shared memory: a sort of the candidates by the 4-word key
+//     (register bitonic, or a rank count up to 64 candidates) -> ord, R and eff by parallel
+//     root walks (shared-memory atomics with early exit, no per-level barriers), and then no
+//     second sort: R by (eff asc, depth desc) is a sequence of chains in ord order (a node y
+//     with eff(y) = ord(y) heads the chain of its ancestors whose eff is ord(y), deepest
+//     first), so a block scan of the chains' bytes places every victim (decide_body.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -246,9 +246,10 @@ __device__ __forceinline__ uint64_t time_order(double t) {
 }
 
 // Shared-memory layout for n <= 4096 nodes (PN = pow2 >= n):
-//   pk0 u64[PN] | pk1 u64[PN]   phase-1 primary keys by position (later: final keys | prefix)
-//   parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | bytes u64[n] | sel u16[PN]
-//   | depth u16[n] | status u8[n] | flags u8[n] | backed u8[n]
+//   pk0 u64[PN] | pk1 u64[PN]   phase-1 primary keys by candidate
+//   parent i32[n] | ord i32[n] | eff i32[n] | blocked u32[n] | bytes u64[n] | id u64[n]
+//   | sel u16[PN] | posn u16[PN] (node at each `before` position) | status u8[n] | flags u8[n]
+//   | backed u8[n]
 // Everything the later phases touch is staged here once, so inputs may live in mapped host
 // memory (small trees) without per-phase PCIe round trips.
 // flags: bit0 selfok, bit1 releases, bit2 R
@@ -260,8 +261,6 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     const uint32_t PN = pow2_ceil(n > 1 ? n : 2);
     uint64_t* pk0 = reinterpret_cast<uint64_t*>(sm);
     uint64_t* pk1 = pk0 + PN;
-    uint64_t* keys = pk0;  // reuse after phase 1
-    uint64_t* pref = pk1;
     int32_t* parent = reinterpret_cast<int32_t*>(pk1 + PN);
     int32_t* ord = parent + n;
     int32_t* eff = ord + n;
@@ -269,11 +268,11 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     uint64_t* nbytes = reinterpret_cast<uint64_t*>(blocked + n);  // offset 16*PN + 16*n: 8-aligned
     uint64_t* nid = nbytes + n;  // node ids: exact-key ties resolve here, not in global memory
     uint16_t* sel = reinterpret_cast<uint16_t*>(nid + n);
-    uint16_t* dep = sel + PN;
-    uint8_t* st = reinterpret_cast<uint8_t*>(dep + n);
+    uint16_t* posn = sel + PN;  // node at each `before` position (phase 2 -> phase 5)
+    uint8_t* st = reinterpret_cast<uint8_t*>(posn + PN);
     uint8_t* flags = st + n;
     uint8_t* bk = flags + n;
-    __shared__ uint32_t s_cnt, s_rcnt, s_slow;
+    __shared__ uint32_t s_cnt, s_slow, s_taken, s_warpn[32];
     __shared__ unsigned long long s_imm, s_pend, s_warp[32], s_stamp[12];
     // per-phase timestamps (globaltimer ns, SM cycles) -> header[3..14] at the end (read by
     // kvf_get_stats); kept in shared memory meanwhile: a store to mapped host memory per phase
@@ -303,7 +302,7 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         t.backed = rebase(t.backed, t.blob, sb);
     }
     if (threadIdx.x == 0) {
-        s_cnt = s_rcnt = s_slow = 0;
+        s_cnt = s_slow = s_taken = 0;
         s_imm = s_pend = 0;
     }
     __syncthreads();
@@ -321,7 +320,6 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         st[i] = s;
         nbytes[i] = bytes;
         nid[i] = t.id[i];
-        if (t.depth) dep[i] = t.depth[i];
         bk[i] = t.backed[i];
         flags[i] = (selfok ? 1 : 0) | (releases ? 2 : 0);
         blocked[i] = 0;
@@ -349,14 +347,6 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
         }
     }
     __syncthreads();
-    if (!t.depth) {  // mirror trees carry no depth (a split would change a whole subtree's):
-                     // count each node's root path in the staged parent array
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            uint32_t d = 0;
-            for (int32_t v = parent[i]; v >= 0; v = parent[v]) ++d;
-            dep[i] = static_cast<uint16_t>(d);
-        }
-    }
     const uint32_t c = s_cnt;
     const uint32_t P = pow2_ceil(c > 1 ? c : 2);
     for (uint32_t i = c + threadIdx.x; i < P; i += blockDim.x) {
@@ -393,14 +383,20 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
             }
         }
         for (uint32_t off = G >> 1; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-        if (q == 0 && i < c) ord[sel[i]] = static_cast<int32_t>(cnt);
+        if (q == 0 && i < c) {
+            ord[sel[i]] = static_cast<int32_t>(cnt);
+            posn[cnt] = sel[i];
+        }
         __syncthreads();
     } else if (P <= 64) {  // keys beyond the exact coarsening: the full comparison
         __syncthreads();
         uint32_t i;
         const uint32_t rk = rank64(
             c, [&](uint32_t a, uint32_t b) { return full_after(sel[b], sel[a]); }, i);
-        if (i != 0xFFFFFFFFu) ord[sel[i]] = static_cast<int32_t>(rk);
+        if (i != 0xFFFFFFFFu) {
+            ord[sel[i]] = static_cast<int32_t>(rk);
+            posn[rk] = sel[i];
+        }
         __syncthreads();
     } else {
         sort_reg<Cand>(
@@ -425,7 +421,10 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
                             __shfl_xor_sync(0xffffffffu, v.s, m)};
             },
             [&](uint32_t pos, const Cand& v) {
-                if (v.s != 0xFFFFu) ord[v.s] = static_cast<int32_t>(pos);
+                if (v.s != 0xFFFFu) {
+                    ord[v.s] = static_cast<int32_t>(pos);
+                    posn[pos] = static_cast<uint16_t>(v.s);
+                }
             });
     }
     stamp(2);
@@ -464,99 +463,108 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     }
     __syncthreads();
     stamp(3);
-    // 5. victims = R sorted by (eff asc, depth desc); keys are unique per node
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const bool r_node = (flags[i] & 4) != 0;
-        const uint32_t k = claim(&s_rcnt, r_node);
-        if (r_node)
-            keys[k] = (static_cast<uint64_t>(eff[i]) << 32) | (static_cast<uint64_t>(0xFFFFu - dep[i]) << 16) | i;
-    }
-    __syncthreads();
-    const uint32_t r = s_rcnt;
-    const uint32_t PR = pow2_ceil(r > 1 ? r : 2);
-    for (uint32_t i = r + threadIdx.x; i < PR; i += blockDim.x) keys[i] = ~0ull;
-    if (PR <= 64) {  // keys are unique: rank sort into the spare pk1 half, then swap roles
-        __syncthreads();
-        const uint32_t G = blockDim.x >> 6;
-        const uint32_t i = threadIdx.x / G, q = threadIdx.x % G;
-        uint32_t cnt = 0;
-        const uint64_t a = i < r ? keys[i] : 0;
-        if (i < r) {
-#pragma unroll 8
-            for (uint32_t j = q; j < r; j += G) cnt += static_cast<uint32_t>(keys[j] < a);
+    // 5. victims = R sorted by (eff asc, depth desc) WITHOUT a second sort: that order is a
+    //    sequence of chains -- a node y in R with eff(y) = ord(y) heads the chain y, parent(y),
+    //    ... of the ancestors whose eff is ord(y), deepest first -- and the chain heads come in
+    //    `before` position order.  Each thread takes a run of positions: chain bytes and member
+    //    counts, a block scan, then every member whose bytes-before is < needed is popped
+    //    (radix_cache.cpp:335) at its place in the order.
+    auto head = [&](uint32_t k, uint32_t* y) {
+        *y = posn[k];
+        return (flags[*y] & 4) && eff[*y] == static_cast<int32_t>(k);
+    };
+    const uint32_t per = (c + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo_k = threadIdx.x * per, hi_k = min(c, (threadIdx.x + 1) * per);
+    uint64_t lb = 0;
+    uint32_t ln = 0;
+    for (uint32_t k = lo_k; k < hi_k; ++k) {
+        uint32_t y;
+        if (!head(k, &y)) continue;
+        for (int32_t cur = static_cast<int32_t>(y);;) {
+            lb += nbytes[cur];
+            ++ln;
+            const int32_t pp = parent[cur];
+            if (pp <= 0 || !(flags[pp] & 4) || eff[pp] != static_cast<int32_t>(k)) break;
+            cur = pp;
         }
-        for (uint32_t off = G >> 1; off; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
-        if (q == 0 && i < r) pref[cnt] = a;
-        __syncthreads();
-        uint64_t* tmp = keys;
-        keys = pref;
-        pref = tmp;
-    } else {
-        sort_reg<uint64_t>(
-            PR, [](uint64_t x, uint64_t y) { return x > y; }, [&](uint32_t i) { return keys[i]; },
-            [&](uint32_t i, uint64_t v) { keys[i] = v; },
-            [](uint64_t v, uint32_t m) { return __shfl_xor_sync(0xffffffffu, v, m); },
-            [&](uint32_t pos, uint64_t v) { keys[pos] = v; });
     }
-    stamp(4);
-    // 6. exclusive byte prefix in victim order (block scan)
-    const uint32_t per = (r + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo_k = threadIdx.x * per, hi_k = min(r, (threadIdx.x + 1) * per);
-    uint64_t local = 0;
-    for (uint32_t k = lo_k; k < hi_k; ++k) local += nbytes[keys[k] & 0xFFFFu];
-    uint64_t inc = local;
+    // 6. exclusive (bytes, members) prefix over the threads' position runs (block scan)
+    uint64_t inc = lb;
+    uint32_t incn = ln;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int off = 1; off < 32; off <<= 1) {
         const uint64_t y = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += y;
+        const uint32_t yn = __shfl_up_sync(0xffffffffu, incn, off);
+        if (lane >= off) {
+            inc += y;
+            incn += yn;
+        }
     }
-    if (lane == 31) s_warp[warp] = inc;
+    if (lane == 31) {
+        s_warp[warp] = inc;
+        s_warpn[warp] = incn;
+    }
     __syncthreads();
     if (warp == 0) {
         uint64_t w = lane < nwarps ? s_warp[lane] : 0;
+        uint32_t wn = lane < nwarps ? s_warpn[lane] : 0;
         for (int off = 1; off < 32; off <<= 1) {
             const uint64_t y = __shfl_up_sync(0xffffffffu, w, off);
-            if (lane >= off) w += y;
+            const uint32_t yn = __shfl_up_sync(0xffffffffu, wn, off);
+            if (lane >= off) {
+                w += y;
+                wn += yn;
+            }
         }
-        if (lane < nwarps) s_warp[lane] = w;
+        if (lane < nwarps) {
+            s_warp[lane] = w;
+            s_warpn[lane] = wn;
+        }
     }
     __syncthreads();
-    uint64_t run = inc - local + (warp ? s_warp[warp - 1] : 0);
-    // 7. victim k is popped iff the bytes freed before it are still < needed (radix_cache.cpp:335)
+    uint64_t run = inc - lb + (warp ? s_warp[warp - 1] : 0);
+    uint32_t idx = incn - ln + (warp ? s_warpn[warp - 1] : 0);
+    // 7. pop: members in order while the bytes freed before them are still < needed
     uint64_t my_imm = 0, my_pend = 0;
-    for (uint32_t k = lo_k; k < hi_k; ++k) {
-        const uint32_t v = static_cast<uint32_t>(keys[k] & 0xFFFFu);
-        const uint64_t bytes = nbytes[v];
-        if (run < q.needed) {
-            uint8_t act;
-            if (!q.offload) act = KVF_ACT_REMOVE;
-            else if (bk[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
-            else if (!(q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap)) act = KVF_ACT_REMOVE;
-            else act = KVF_ACT_OFFLOAD;
-            o.idx[k] = static_cast<int32_t>(v);
-            o.action[k] = act;
-            (act == KVF_ACT_OFFLOAD ? my_pend : my_imm) += bytes;
-            pref[k] = 1;
-        } else {
-            pref[k] = 0;
+    uint32_t taken = 0;
+    for (uint32_t k = lo_k; k < hi_k && run < q.needed; ++k) {
+        uint32_t y;
+        if (!head(k, &y)) continue;
+        for (int32_t cur = static_cast<int32_t>(y);;) {
+            const uint32_t v = static_cast<uint32_t>(cur);
+            const uint64_t bytes = nbytes[v];
+            if (run < q.needed) {
+                uint8_t act;
+                if (!q.offload) act = KVF_ACT_REMOVE;
+                else if (bk[v]) act = KVF_ACT_DISCARD_TO_BACKUP;
+                else if (!(q.cpu_cap == 0 || q.cpu_used + bytes <= q.cpu_cap)) act = KVF_ACT_REMOVE;
+                else act = KVF_ACT_OFFLOAD;
+                o.idx[idx] = static_cast<int32_t>(v);
+                o.action[idx] = act;
+                (act == KVF_ACT_OFFLOAD ? my_pend : my_imm) += bytes;
+                taken = idx + 1;
+            }
+            run += bytes;
+            ++idx;
+            const int32_t pp = parent[cur];
+            if (pp <= 0 || !(flags[pp] & 4) || eff[pp] != static_cast<int32_t>(k)) break;
+            cur = pp;
         }
-        run += bytes;
     }
     for (int off = 16; off; off >>= 1) {  // one shared atomic per warp
         my_imm += __shfl_xor_sync(0xffffffffu, my_imm, off);
         my_pend += __shfl_xor_sync(0xffffffffu, my_pend, off);
+        taken = max(taken, __shfl_xor_sync(0xffffffffu, taken, off));
     }
     if (lane == 0) {
         if (my_imm) atomicAdd(&s_imm, static_cast<unsigned long long>(my_imm));
         if (my_pend) atomicAdd(&s_pend, static_cast<unsigned long long>(my_pend));
+        if (taken) atomicMax(&s_taken, taken);
     }
+    stamp(4);
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t lo = 0, hi = r;  // taken victims form a prefix
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (pref[mid]) lo = mid + 1; else hi = mid;
-        }
+        const uint32_t lo = s_taken;  // taken victims form a prefix of the order
         o.header[0] = lo;
         o.header[1] = s_imm;
         o.header[2] = s_pend;
@@ -570,7 +578,7 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
 
 inline size_t victim_smem(uint32_t n, size_t blob = 0) {
     const size_t PN = pow2_ceil(n > 1 ? n : 2);
-    return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 16 + PN * 2 + static_cast<size_t>(n) * 2 +
+    return PN * 16 + static_cast<size_t>(n) * 16 + 8 + static_cast<size_t>(n) * 16 + PN * 2 + PN * 2 +
            3 * ((n + 15) & ~15u) + 64 + (blob ? blob + 32 : 0);
 }
 
