@@ -370,8 +370,9 @@ __device__ __forceinline__ void victim_body(const TreeDev& t_in, const ReqDev& q
     if (P <= 64 && !slow) {  // small trees: rank sort straight into ord, branch-free compares
         __syncthreads();
         // element i's key in registers; G lanes split the others and add up how many precede
-        // it.  The words are exact: a tie is equal (rank, time, seq) and the id decides.
-        const uint32_t G = blockDim.x >> 6;
+        // it.  The words are exact: a tie is equal (rank, time, seq) and the id decides.  G is
+        // as wide as the candidate count allows (<= 32 lanes: the reduction stays in a warp)
+        const uint32_t G = min(32u, blockDim.x / P);
         const uint32_t i = threadIdx.x / G, q = threadIdx.x % G;
         uint32_t cnt = 0;
         if (i < c) {

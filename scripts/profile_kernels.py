@@ -57,7 +57,7 @@ def main(which):
             e.victims(tree, c["needed"], c["policy"], c["mode"], c["has_floor"], c["floor"], c["cpu_used"],
                       c["cpu_cap"])
         print("k5 nodes", ta.n)
-    if which in ("k5mirror", "k5big"):
+    if which in ("k5mirror", "k5big", "k5mirrorsmall"):
         # K5 over the HBM mirror: a 1.4k-node golden tree (one-shot kvf_decide_once; run with
         # KVF_DECIDER=0 so no resident CTA is in the capture) or a 30k-node tree on the
         # hand-written device-wide path (big_* kernels)
@@ -66,6 +66,9 @@ def main(which):
         from paper_2507_07400_b200.engine import Tree
         if which == "k5mirror":
             c = sorted(load_jsonl("evict_medium.jsonl"), key=lambda c: -len(c["parent"]))[0]
+        elif which == "k5mirrorsmall":  # a BASELINE-sized tree (~44 nodes, like C1/C2)
+            c = min((x for x in load_jsonl("evict_small.jsonl") if "error" not in x),
+                    key=lambda c: abs(len(c["parent"]) - 44))
         else:
             import json
             out = subprocess.run([os.path.join(ORACLE_DIR, "_ref", "ref_trace"), "evict", "seed=7", "cases=1",
