@@ -382,7 +382,8 @@ def run_ours(args, rank, world, local):
                 "lockstep_k1_gbs": round(res["prefetch_bytes"] / (res["prefetch_device_ms"] * 1e-3) / 1e9, 3)
                 if res["prefetch_device_ms"] else None,
                 "breakdown_ms": {"arrival_decisions": round(res["decision_us_total"] / 1e3, 2),
-                                 "k4_calls": res["priority_calls"], "k4_total": round(res["priority_us"] / 1e3, 2),
+                                 "k4_calls": res["priority_calls"], "k4_issued": res["priority_issued"],
+                                 "k4_total": round(res["priority_us"] / 1e3, 2),
                                  "k5_calls": res["evict_calls"], "k5_total": round(res["evict_us"] / 1e3, 2),
                                  "fence_wait": round(res["fence_wait_us"] / 1e3, 2),
                                  "h2d_device": round((res["prefetch_device_ms"] + res["reactive_device_ms"]), 2),
@@ -394,6 +395,10 @@ def run_ours(args, rank, world, local):
                 "decider": {"resident_served": res["resident_served"], "oneshot_served": res["oneshot_served"],
                             "resident_launches": res["resident_launches"], "mirror_records": res["mirror_records"]}},
         "latency": {"decision_us_per_agent_step": round(res["decision_us_total"] / steps_e2e, 2),
+                    # the same arrivals without the launch + stop event of their real K1 / K2
+                    # (the reference's decisions book transfers in a ledger and move no bytes)
+                    "decision_excl_transfer_issue_us_per_agent_step":
+                        round((res["decision_us_total"] - res["decision_issue_us"]) / steps_e2e, 2),
                     "decision_us_max": round(res["decision_us_max"], 2),
                     "k4_us_per_call": round(res["priority_us"] / max(1, res["priority_calls"]), 2),
                     "k5_us_per_call": round(res["evict_us"] / max(1, res["evict_calls"]), 2),

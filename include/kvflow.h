@@ -252,6 +252,9 @@ typedef struct kvf_tree kvf_tree;
 
 #define KVF_SLOT_DEAD 0xFF        /* status of a freed slot */
 #define KVF_RESIDENT_MAX_SLOTS 128u
+/* Record flag: the host has not read back a queued K4 yet, so its copy of this node's rank may
+ * be stale -- the record updates every other field and keeps the rank the mirror holds. */
+#define KVF_REC_KEEP_RANK 1u
 
 typedef struct {
     uint32_t slot;    /* mirror slot of this node */
@@ -259,7 +262,7 @@ typedef struct {
     int32_t lock;     /* lock_count (radix_cache.hpp:57) */
     uint8_t status;   /* NodeStatus 0..3, or KVF_SLOT_DEAD */
     uint8_t backed;   /* cpu_backed */
-    uint16_t pad0;
+    uint16_t flags;   /* KVF_REC_KEEP_RANK: leave the mirror's rank as it is (see below) */
     int64_t rank;     /* host-authored ranks (new nodes SUFFIX, split halves); K4 rewrites them */
     double time;      /* LastAccess.time */
     uint64_t seq;     /* LastAccess.seq */
@@ -280,8 +283,10 @@ int kvf_tree_update(kvf_tree* t, const kvf_node_rec* recs, uint32_t n);
 int kvf_tree_set_hints(kvf_tree* t, uint32_t hints);
 /* K4 over the mirror (set_agent_priorities): boundary_slot[b] / cand_rank[b] as for
  * kvf_priority_propagate.  Asynchronous: returns once the request is queued; the mirror's
- * ranks are updated before any later decision on this tree.  kvf_tree_rank_changes waits for
- * it and returns the slots whose rank changed (at most the tree's slot count entries). */
+ * ranks are updated before any later decision on this tree.  Up to two K4 requests may be
+ * outstanding (KVF_E_INVALID_ARG for a third); kvf_tree_rank_changes waits for the OLDEST and
+ * returns the slots whose rank it changed (at most the tree's slot count entries), relative
+ * to the ranks the K4 before it left -- applying each result in order gives the latest ranks. */
 int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m);
 int kvf_tree_rank_changes(kvf_tree* t, uint32_t* slots, int64_t* ranks, uint32_t cap, uint32_t* n_changed);
 /* K5 over the mirror (evict's victim order and actions); victims as slots.  Synchronous. */

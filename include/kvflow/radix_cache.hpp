@@ -74,6 +74,7 @@ struct CacheNode {
     RadixCache* owner = nullptr;  // the cache whose mirror holds this node
     uint32_t slot = 0;            // its mirror slot (root: 0)
     bool mirror_dirty = false;    // changed since the mirror last heard of it
+    uint64_t k4_born = 0;         // K4 requests posted before this node took its slot
 
     size_t token_count() const { return key.size(); }
     bool is_root() const { return parent == nullptr; }
@@ -146,11 +147,16 @@ public:
 
     // K4 on the GPU: every node SUFFIX, then min(rank_for_step) along boundary root paths.
     void set_agent_priorities(const StepMap& steps);
-    // The same, queued: returns once the request is on the decision ring.  The nodes' ranks
-    // are updated by join_priorities(), which insert / mark_fixed_boundary / evict call first
-    // (a split copies the rank, an evict applies victims); until then node.rank is the old one.
+    // The same, deferred: the boundaries and candidates are captured now and the K4 runs on
+    // the GPU ahead of the tree's next K5 (in the same ring slot), or when join_priorities()
+    // needs the ranks (observers, dump, the end of a run); a newer call replaces a captured one
+    // no reader needed (every K4 recomputes all ranks from scratch).  The host nodes get the
+    // ranks from join_priorities(); insert / mark_fixed_boundary read back issued ones first
+    // (a split copies the rank).  Until then node.rank is the old one, and the records shipped
+    // for nodes that existed when a K4 was issued keep the mirror's rank (KVF_REC_KEEP_RANK).
     void set_agent_priorities_async(const StepMap& steps);
     void join_priorities();
+    bool priorities_pending() const { return k4_deferred_ || k4_posts_ > k4_joined_; }
     // A node's mirrored fields changed outside the cache (TierManager: status, cpu_backed).
     void note_changed(CacheNode& n);
     // K5 on the GPU picks the ordered victims; the host applies each action through `tier`.
@@ -178,6 +184,7 @@ public:
     // records; records = node records shipped to the mirror).
     struct DecisionStats {
         uint64_t priority_calls = 0, evict_calls = 0, records = 0;
+        uint64_t priority_issued = 0;  // K4s that ran on the GPU (the rest were replaced unread)
         double priority_us = 0, evict_us = 0, pack_us = 0;
         double k4_join_us = 0;  // waiting for queued K4 results (its post is priority_us - this)
         double k5_us = 0;       // inside kvf_tree_victims (post + wait + copy-out)
@@ -200,7 +207,6 @@ private:
     void stamp(CacheNode& n, VirtualTime now);
     kvf_tree* tree();                 // created on first use (the engine may be attached late)
     void flush_records();
-    void post_priorities(const StepMap& steps);
 
     Bytes bpt_;
     Engine* engine_ = nullptr;
@@ -217,11 +223,19 @@ private:
     std::vector<uint32_t> free_slots_;     // min-heap: slots stay dense
     std::vector<uint32_t> freed_pending_;  // freed since the last decision: reusable after it
     std::vector<uint32_t> dirty_;          // slots to ship with the next decision
+    std::vector<uint32_t> bslot_;          // K4 request staging (boundary slots, candidate ranks)
+    std::vector<int64_t> cand_;
     std::vector<kvf_node_rec> recs_;
     std::vector<uint32_t> chg_slot_, vic_slot_;
     std::vector<int64_t> chg_rank_;
     std::vector<uint8_t> vic_act_;
-    bool k4_pending_ = false;
+    // K4 requests issued to the engine / read back so far; the ones in between are queued (at
+    // most two, the engine's result buffers), numbered k4_joined_ + 1 .. k4_posts_
+    uint64_t k4_posts_ = 0, k4_joined_ = 0;
+    bool k4_deferred_ = false;  // a captured K4 (bslot_ / cand_) not issued yet
+    void issue_priorities();
+    void join_oldest_priorities();
+    void join_issued_priorities();
     bool time_follows_seq_ = true;          // every stamp so far had a non-decreasing time
     uint32_t hints_sent_ = ~0u;
     VirtualTime last_stamp_ = -std::numeric_limits<double>::infinity();

@@ -88,6 +88,11 @@ typedef struct {
     /* host-time breakdown (us): waiting for queued K4 results, K5 calls, applying victims
        (ledger + K2 issue), issuing K1/K2 on the engine */
     double k4_join_us, k5_us, apply_us, issue_us;
+    /* the part of decision_us_total spent issuing K1 / K2 (launch + stop event) inside arrivals:
+       real byte movement the reference's ledger-only decisions do not have */
+    double decision_issue_us;
+    /* K4 calls that ran on the GPU (priority_calls minus the ones a newer call replaced unread) */
+    uint64_t priority_issued;
 } kvfh_sim_result;
 
 const char* kvfh_last_error(void);

@@ -37,7 +37,8 @@ class SimResult(C.Structure):
         ("engine_decision_call_us", C.c_double),
         ("resident_served", C.c_uint64), ("oneshot_served", C.c_uint64), ("resident_launches", C.c_uint64),
         ("mirror_records", C.c_uint64), ("k4_join_us", C.c_double), ("k5_us", C.c_double), ("apply_us", C.c_double),
-        ("issue_us", C.c_double),
+        ("issue_us", C.c_double), ("decision_issue_us", C.c_double),
+        ("priority_issued", C.c_uint64),
     ]
 
 

@@ -71,7 +71,7 @@ class Stats(C.Structure):
 
 class NodeRec(C.Structure):  # kvf_node_rec
     _fields_ = [("slot", C.c_uint32), ("parent", C.c_int32), ("lock", C.c_int32), ("status", C.c_uint8),
-                ("backed", C.c_uint8), ("pad0", C.c_uint16), ("rank", C.c_int64), ("time", C.c_double),
+                ("backed", C.c_uint8), ("flags", C.c_uint16), ("rank", C.c_int64), ("time", C.c_double),
                 ("seq", C.c_uint64), ("id", C.c_uint64), ("tokens", C.c_uint64), ("pad1", C.c_uint64)]
 
 

@@ -192,6 +192,7 @@ int kvfh_sim_create(const kvfh_sim_config* c, kvfh_sim** out) {
             if (prev) prev(n, from, to);
         };
         const bool audit = c->audit != 0;
+        s->sim->observe_ranks = audit;
         s->sim->post_event_hook = [raw, audit](VirtualTime) {
             if (audit) {
                 raw->sim->tier().audit(raw->sim->cache());
@@ -292,6 +293,8 @@ int kvfh_sim_result_get(const kvfh_sim* s, kvfh_sim_result* r) {
         r->k5_us = d.k5_us;
         r->apply_us = d.apply_us;
         r->issue_us = s->sim->tier().issue_us();
+        r->decision_issue_us = h.decision_issue_us;
+        r->priority_issued = d.priority_issued;
         r->verified_loads = s->sim->verified_loads;
         r->verify_failures = s->sim->verify_failures;
         r->audits = s->audits;

@@ -43,7 +43,7 @@ constexpr size_t kSlotBytes = 512;     // one warp reads a slot in one round: 32
 constexpr size_t kHdrBytes = 128;
 constexpr size_t kInlineBytes = kSlotBytes - kHdrBytes;  // records + boundaries travel in the slot
 constexpr size_t kPaySlotBytes = 256u << 10;  // per ring slot, for batches that do not fit inline
-enum : uint32_t { REQ_PRIO = 1, REQ_VICTIMS = 2, REQ_APPLY = 3 };
+enum : uint32_t { REQ_PRIO = 1, REQ_VICTIMS = 2, REQ_APPLY = 3, REQ_PRIO_VICTIMS = 4 };  // 4: K4 then K5, one slot
 
 struct MirrorDev {
     int32_t* parent;
@@ -60,9 +60,10 @@ struct MirrorDev {
 struct TreeDesc {  // device memory, per tree (rewritten only when its mirror is reallocated)
     MirrorDev mir;
     long long* scratch;           // K4 ranks above the shared-memory limit
-    unsigned long long* out_k4;   // result headers (mapped pinned); results from + 128 B
+    unsigned long long* out_k4;   // K4 result buffer 0 (mapped pinned); results from + 128 B
     unsigned long long* out_k5;
     uint64_t bpt;
+    uint64_t k4_stride;           // bytes from K4 result buffer 0 to buffer 1
 };
 
 // A ring slot.  The host writes the body, then `hash` (over seq and bytes 16..511), then `seq`
@@ -79,7 +80,8 @@ struct DecReq {
     uint64_t needed;
     int64_t floor;
     uint64_t cpu_used, cpu_cap;
-    int32_t wa, offload, has_floor, pad;
+    int32_t wa, offload, has_floor;
+    uint32_t k4_buf;  // K4: which of the tree's two result buffers it writes
 };
 static_assert(sizeof(DecReq) <= kHdrBytes, "request header");
 union alignas(16) ReqSlot {
@@ -140,7 +142,22 @@ __device__ __forceinline__ bool read_slot(ReqSlot& dst, const ReqSlot* src, unsi
 
 // Node records -> mirror (last record of a slot wins: the host sends one per slot per batch);
 // inline records come from the slot copy in shared memory, others from host / device memory
-__device__ __forceinline__ void apply_records(const DecReq& q, const MirrorDev& mir, const ReqSlot& slot) {
+__device__ __forceinline__ void put_rec(const MirrorDev& mir, uint32_t s, const uint4& a, const uint4& b, const uint4& c,
+                                        const uint4& d) {
+    mir.parent[s] = static_cast<int32_t>(a.y);
+    mir.lock[s] = static_cast<int32_t>(a.z);
+    mir.status[s] = static_cast<uint8_t>(a.w & 0xFF);
+    mir.backed[s] = static_cast<uint8_t>((a.w >> 8) & 0xFF);
+    if (!((a.w >> 16) & KVF_REC_KEEP_RANK)) mir.rank[s] = static_cast<int64_t>((static_cast<uint64_t>(b.y) << 32) | b.x);
+    mir.time[s] = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(b.w) << 32) | b.z));
+    mir.seq[s] = (static_cast<uint64_t>(c.y) << 32) | c.x;
+    mir.id[s] = (static_cast<uint64_t>(c.w) << 32) | c.z;
+    mir.tokens[s] = (static_cast<uint64_t>(d.y) << 32) | d.x;
+}
+
+// cm (nullable): the resident CTA's shared-memory copy of the tree, updated alongside HBM
+__device__ __forceinline__ void apply_records(const DecReq& q, const MirrorDev& mir, const MirrorDev* cm,
+                                              const ReqSlot& slot) {
     const bool inl = q.recs == nullptr;
     for (uint32_t i = threadIdx.x; i < q.n_recs; i += blockDim.x) {
         uint4 a, b, c, d;
@@ -157,32 +174,56 @@ __device__ __forceinline__ void apply_records(const DecReq& q, const MirrorDev& 
             c = __ldcv(p + 2);
             d = __ldcv(p + 3);
         }
-        const uint32_t s = a.x;
-        mir.parent[s] = static_cast<int32_t>(a.y);
-        mir.lock[s] = static_cast<int32_t>(a.z);
-        mir.status[s] = static_cast<uint8_t>(a.w & 0xFF);
-        mir.backed[s] = static_cast<uint8_t>((a.w >> 8) & 0xFF);
-        mir.rank[s] = static_cast<int64_t>((static_cast<uint64_t>(b.y) << 32) | b.x);
-        mir.time[s] = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(b.w) << 32) | b.z));
-        mir.seq[s] = (static_cast<uint64_t>(c.y) << 32) | c.x;
-        mir.id[s] = (static_cast<uint64_t>(c.w) << 32) | c.z;
-        mir.tokens[s] = (static_cast<uint64_t>(d.y) << 32) | d.x;
+        put_rec(mir, a.x, a, b, c, d);
+        if (cm) put_rec(*cm, a.x, a, b, c, d);
     }
     __syncthreads();
+}
+
+// Slots [from, to) of the HBM mirror -> the shared-memory copy.
+__device__ __forceinline__ void load_cache(const MirrorDev& mir, const MirrorDev& cm, uint32_t from, uint32_t to) {
+    for (uint32_t i = from + threadIdx.x; i < to; i += blockDim.x) {
+        cm.parent[i] = mir.parent[i];
+        cm.lock[i] = mir.lock[i];
+        cm.status[i] = mir.status[i];
+        cm.backed[i] = mir.backed[i];
+        cm.rank[i] = mir.rank[i];
+        cm.time[i] = mir.time[i];
+        cm.seq[i] = mir.seq[i];
+        cm.id[i] = mir.id[i];
+        cm.tokens[i] = mir.tokens[i];
+    }
+}
+
+// The shared-memory copy of a tree of up to `cap` slots, placed at `base`: 50 B per slot.
+__device__ __forceinline__ MirrorDev cache_view(uint8_t* base, uint32_t cap) {
+    MirrorDev m;
+    m.rank = reinterpret_cast<int64_t*>(base);
+    m.time = reinterpret_cast<double*>(m.rank + cap);
+    m.seq = reinterpret_cast<uint64_t*>(m.time + cap);
+    m.id = m.seq + cap;
+    m.tokens = m.id + cap;
+    m.parent = reinterpret_cast<int32_t*>(m.tokens + cap);
+    m.lock = m.parent + cap;
+    m.status = reinterpret_cast<uint8_t*>(m.lock + cap);
+    m.backed = m.status + cap;
+    return m;
 }
 
 // K4 over the mirror (radix_cache.cpp:266-285): SUFFIX everywhere, then each boundary's
 // candidate min-reduced along its root path; ranks that differ from the mirror's are written
 // back to it and reported as (slot, rank) changes.
-__device__ __forceinline__ void prio_body(const DecReq& q, const TreeDesc& td, const ReqSlot& slot) {
+// rd: where the tree is read (the resident CTA's shared-memory copy, or HBM); changed ranks are
+// written to HBM and to rd.
+__device__ __forceinline__ void prio_body(const DecReq& q, const TreeDesc& td, const MirrorDev& rd, const ReqSlot& slot) {
     extern __shared__ __align__(16) uint8_t sm[];
     __shared__ uint32_t s_cnt;
     const MirrorDev& mir = td.mir;
     const uint32_t n = q.n;
     const bool staged = n <= kPrioSmemNodes;
     long long* r = staged ? reinterpret_cast<long long*>(sm) : td.scratch;
-    const int32_t* par = mir.parent;
-    if (staged) {
+    const int32_t* par = rd.parent;
+    if (staged && rd.parent == mir.parent) {
         int32_t* ps = reinterpret_cast<int32_t*>(sm + n * 8ull);
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) ps[i] = mir.parent[i];
         par = ps;
@@ -206,15 +247,17 @@ __device__ __forceinline__ void prio_body(const DecReq& q, const TreeDesc& td, c
         for (; v > 0; v = par[v]) atomicMin(r + v, c);
     }
     __syncthreads();
-    unsigned long long* out = td.out_k4;
+    unsigned long long* out =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(td.out_k4) + q.k4_buf * td.k4_stride);
     uint32_t* o_slot = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(out) + kHeaderBytes);
     int64_t* o_rank = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(out) + kHeaderBytes + ((n * 4ull + 15) & ~15ull));
     for (uint32_t i = threadIdx.x + 1; i < n; i += blockDim.x) {
         const long long v = r[i];
-        const bool ch = mir.status[i] != KVF_SLOT_DEAD && v != mir.rank[i];
+        const bool ch = rd.status[i] != KVF_SLOT_DEAD && v != rd.rank[i];
         const uint32_t k = claim(&s_cnt, ch);
         if (ch) {
             mir.rank[i] = v;
+            rd.rank[i] = v;
             o_slot[k] = i;
             o_rank[k] = v;
         }
@@ -225,18 +268,18 @@ __device__ __forceinline__ void prio_body(const DecReq& q, const TreeDesc& td, c
 
 // K5 over the mirror: the snapshot kernel's body (decide_body.cuh) reading the HBM arrays in
 // place, depth recomputed from the parents.
-__device__ __forceinline__ void victims_body(const DecReq& q, const TreeDesc& td) {
+__device__ __forceinline__ void victims_body(const DecReq& q, const TreeDesc& td, const MirrorDev& rd) {
     TreeDev t;
-    t.parent = td.mir.parent;
+    t.parent = rd.parent;
     t.depth = nullptr;
-    t.status = td.mir.status;
-    t.lock = td.mir.lock;
-    t.rank = td.mir.rank;
-    t.time = td.mir.time;
-    t.seq = td.mir.seq;
-    t.id = td.mir.id;
-    t.tokens = td.mir.tokens;
-    t.backed = td.mir.backed;
+    t.status = rd.status;
+    t.lock = rd.lock;
+    t.rank = rd.rank;
+    t.time = rd.time;
+    t.seq = rd.seq;
+    t.id = rd.id;
+    t.tokens = rd.tokens;
+    t.backed = rd.backed;
     t.n = q.n;
     t.bpt = td.bpt;
     t.blob = nullptr;
@@ -250,20 +293,43 @@ __device__ __forceinline__ void victims_body(const DecReq& q, const TreeDesc& td
     victim_body(t, rq, o, 0);
 }
 
-__device__ __forceinline__ void serve(const ReqSlot& slot, Ctl* ctl, unsigned long long seq, unsigned long long polls) {
-    __shared__ TreeDesc td;
+// The CTA's state across requests: the descriptor of the tree it served last and, for the
+// resident CTA, how many of that tree's slots its shared-memory copy holds.  While a resident
+// CTA lives it is the only writer of the small trees' mirrors (a request for any other
+// executor stops it first; a mirror reallocation drains it), so the copy stays equal to HBM.
+struct ServeState {
+    TreeDesc td;
+    const TreeDesc* tree;  // nullptr: nothing cached
+    uint32_t cached_n;
+};
+
+__device__ __forceinline__ void serve(const ReqSlot& slot, Ctl* ctl, unsigned long long seq, unsigned long long polls,
+                                      ServeState& ss, const MirrorDev* cm) {
     __shared__ unsigned long long s_seen;
     if (threadIdx.x == 0) s_seen = gtimer();
     const DecReq& q = slot.r;
-    if (threadIdx.x < sizeof(TreeDesc) / 8)
-        reinterpret_cast<uint64_t*>(&td)[threadIdx.x] = reinterpret_cast<const uint64_t*>(q.tree)[threadIdx.x];
+    const bool fresh = q.tree != ss.tree;  // (read by every thread before the barrier below)
+    const uint32_t have = fresh ? 0u : ss.cached_n;
+    if (fresh && threadIdx.x < sizeof(TreeDesc) / 8)  // a dependent HBM read: once per tree
+        reinterpret_cast<uint64_t*>(&ss.td)[threadIdx.x] = reinterpret_cast<const uint64_t*>(q.tree)[threadIdx.x];
     // a batch that did not fit the slot sits in the payload area: order those reads after the
     // slot's (the host wrote it first)
     if (q.recs || q.bslot) asm volatile("fence.acq_rel.sys;" ::: "memory");
     __syncthreads();
-    apply_records(q, td.mir, slot);
-    if (q.type == REQ_PRIO) prio_body(q, td, slot);
-    else if (q.type == REQ_VICTIMS) victims_body(q, td);
+    const TreeDesc& td = ss.td;
+    if (cm && q.n > have) {  // a new tree, or slots it grew into: from HBM once
+        load_cache(td.mir, *cm, have, q.n);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ss.tree = cm ? q.tree : nullptr;
+        ss.cached_n = cm ? max(q.n, have) : 0u;
+    }
+    apply_records(q, td.mir, cm, slot);
+    const MirrorDev& rd = cm ? *cm : td.mir;
+    if (q.type == REQ_PRIO || q.type == REQ_PRIO_VICTIMS) prio_body(q, td, rd, slot);
+    if (q.type == REQ_PRIO_VICTIMS) __syncthreads();  // the K5 reads the ranks the K4 wrote
+    if (q.type == REQ_VICTIMS || q.type == REQ_PRIO_VICTIMS) victims_body(q, td, rd);
     if (threadIdx.x == 0) {  // diagnostics (KVF_MIRROR_TRACE)
         ctl->t_seen[seq % kRing] = s_seen;
         ctl->t_done[seq % kRing] = gtimer();
@@ -286,18 +352,35 @@ __global__ void __launch_bounds__(kThreads) kvf_decide_once(const ReqSlot* slot,
         while (!read_slot(req, slot, seq, nullptr, nullptr)) ++polls;
         if (threadIdx.x == 0) s_polls = polls;
     }
+    __shared__ ServeState ss;
+    if (threadIdx.x == 0) ss.tree = nullptr;
     __syncthreads();
-    serve(req, ctl, seq, s_polls);
+    serve(req, ctl, seq, s_polls, ss, nullptr);
+}
+
+// scratch of the decision bodies for trees of up to `cap` slots (16-B multiple)
+inline size_t resident_scratch(uint32_t cap) {
+    const size_t v = victim_smem(cap), p = static_cast<size_t>(cap) * 12 + 64;
+    return ((v > p ? v : p) + 15) & ~size_t(15);
 }
 
 // The resident decider: serves ring requests first, first+1, ... until idle_ns pass without
 // one or the host raises stop_epoch to this launch's epoch; then publishes where it stopped.
 __global__ void __launch_bounds__(kResThreads, 4) kvf_decider_kernel(ReqSlot* ring, Ctl* ctl, unsigned long long first,
                                                                       unsigned long long epoch,
-                                                                      unsigned long long idle_ns) {
+                                                                      unsigned long long idle_ns, uint32_t cap,
+                                                                      uint32_t cache_off) {
+    extern __shared__ __align__(16) uint8_t sm[];
     __shared__ ReqSlot req;
     __shared__ int s_go;
     __shared__ unsigned long long s_polls;
+    __shared__ ServeState ss;
+    // the tree copy sits after the decision bodies' scratch (cache_off = resident_scratch(cap))
+    const MirrorDev cm = cache_view(sm + cache_off, cap);
+    if (threadIdx.x == 0) {
+        ss.tree = nullptr;
+        ss.cached_n = 0;
+    }
     unsigned long long next = first;
     unsigned long long last = gtimer();
     for (;;) {
@@ -320,7 +403,7 @@ __global__ void __launch_bounds__(kResThreads, 4) kvf_decider_kernel(ReqSlot* ri
         }
         __syncthreads();
         if (!s_go) break;
-        serve(req, ctl, next, s_polls);
+        serve(req, ctl, next, s_polls, ss, &cm);
         ++next;
         last = gtimer();
         __syncthreads();  // s_go / req are rewritten next round
@@ -332,8 +415,9 @@ __global__ void __launch_bounds__(kResThreads, 4) kvf_decider_kernel(ReqSlot* ri
     }
 }
 
-// shared memory of a resident CTA serving trees of up to `cap` slots
-size_t resident_smem(uint32_t cap) { return std::max(victim_smem(cap), static_cast<size_t>(cap) * 12 + 64); }
+// shared memory of a resident CTA serving trees of up to `cap` slots: the decision bodies'
+// scratch, then the tree's shared-memory copy (50 B per slot)
+size_t resident_smem(uint32_t cap) { return resident_scratch(cap) + static_cast<size_t>(cap) * 50; }
 // a resident CTA is sized to the tree it serves (a 44-node tree needs ~3 KB, 512 slots ~25 KB)
 uint32_t resident_cap(uint32_t n) {
     uint32_t c = 64;
@@ -368,8 +452,17 @@ struct kvf_tree {
     kvf_node_rec* bulk = nullptr;  // device copy of record batches too big for a ring slot
     size_t bulk_cap = 0;
     std::vector<kvf_node_rec> staged;
-    uint64_t k4_seq = 0;  // outstanding K4 request
-    uint32_t k4_n = 0;
+    // outstanding K4 requests (at most two, oldest at k4_head): sequence number, slot count
+    uint64_t k4_seq[2] = {0, 0};
+    uint32_t k4_n[2] = {0, 0};
+    uint32_t k4_head = 0, k4_count = 0;  // (count includes a staged K4)
+    size_t k4_stride = 0;
+    // the newest K4, staged on the host until the tree's next request: it travels in the same
+    // ring slot as the next K5 (one poll, one serve) or goes alone before any other reader
+    bool k4_staged = false;
+    uint32_t k4_staged_buf = 0;
+    std::vector<uint32_t> k4_bslot;
+    std::vector<int64_t> k4_cand;
     kvf_impl::LargeState large;
     kvf_impl::LargeKeyInfo keys;
 };
@@ -388,9 +481,10 @@ int launch_once(kvf_engine* e, uint64_t seq) {
     const DecReq& q = ring_slot(d.ring_h, seq)->r;
     uint32_t threads = kThreads;
     size_t smem = 0;
-    if (q.type == REQ_VICTIMS) {
+    if (q.type == REQ_VICTIMS || q.type == REQ_PRIO_VICTIMS) {
         threads = victim_threads(q.n);
         smem = victim_smem(q.n);
+        if (q.type == REQ_PRIO_VICTIMS) smem = std::max<size_t>(smem, q.n * 12ull + 64);
     } else if (q.type == REQ_PRIO) {
         threads = std::min<uint32_t>(kThreads, std::max<uint32_t>(128, pow2_ceil(std::max(q.n, q.m))));
         smem = q.n <= kPrioSmemNodes ? q.n * 12ull + 64 : 0;
@@ -423,7 +517,7 @@ int launch_resident(kvf_engine* e, uint64_t first) {
     ++d.epoch;
     kvf_decider_kernel<<<1, kResThreads, resident_smem(d.res_cap), d.s_res>>>(
         reinterpret_cast<ReqSlot*>(d.ring_d), reinterpret_cast<Ctl*>(ring_ctl(d.ring_d)), first, d.epoch,
-        d.hold ? ~0ull : d.idle_ns);
+        d.hold ? ~0ull : d.idle_ns, d.res_cap, static_cast<uint32_t>(resident_scratch(d.res_cap)));
     KVF_CUDA(cudaGetLastError());
     d.running = true;
     e->stats.kernel_launches++;
@@ -549,9 +643,12 @@ int ensure_cap(kvf_tree* t, uint32_t need) {
     uint32_t cap = std::max<uint32_t>(need + need / 2, 1024);
     cap = large_capacity(cap);
     if (int rc = drain(e)) return rc;
-    // an unread K4 result lives in the output block being replaced: carry it over
-    std::vector<char> k4_keep;
-    if (t->k4_seq && t->out_h) k4_keep.assign(t->out_h, t->out_h + k4_out_bytes(t->k4_n));
+    // unread K4 results live in the output block being replaced: carry them over
+    std::vector<char> k4_keep[2];
+    for (uint32_t b = 0; b < 2; ++b)
+        for (uint32_t k = 0; k < t->k4_count; ++k)
+            if ((t->k4_head + k) % 2 == b && t->out_h)
+                k4_keep[b].assign(t->out_h + b * t->k4_stride, t->out_h + b * t->k4_stride + k4_out_bytes(t->k4_n[b]));
     const size_t n = cap;
     auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
     const size_t bytes = al(n * 4) * 2 + al(n) * 2 + al(n * 8) * 6;
@@ -592,25 +689,27 @@ int ensure_cap(kvf_tree* t, uint32_t need) {
     // results: posted writes into mapped pinned memory
     if (t->out_h) cudaFreeHost(t->out_h);
     t->out_h = t->out_d = nullptr;
-    t->k5_off = (k4_out_bytes(cap) + 255) & ~size_t(255);
+    t->k4_stride = (k4_out_bytes(cap) + 255) & ~size_t(255);
+    t->k5_off = 2 * t->k4_stride;
     void* h = nullptr;
     KVF_CUDA(cudaHostAlloc(&h, t->k5_off + k5_out_bytes(cap), cudaHostAllocMapped | cudaHostAllocPortable));
     void* dp = nullptr;
     KVF_CUDA(cudaHostGetDevicePointer(&dp, h, 0));
     t->out_h = static_cast<char*>(h);
     t->out_d = static_cast<char*>(dp);
-    if (!k4_keep.empty()) std::memcpy(t->out_h, k4_keep.data(), k4_keep.size());
+    for (uint32_t b = 0; b < 2; ++b)
+        if (!k4_keep[b].empty()) std::memcpy(t->out_h + b * t->k4_stride, k4_keep[b].data(), k4_keep[b].size());
     t->cap = cap;
     if (!t->desc) KVF_CUDA(cudaMalloc(reinterpret_cast<void**>(&t->desc), sizeof(TreeDesc)));
     TreeDesc td{t->mir, t->scratch, reinterpret_cast<unsigned long long*>(t->out_d),
-                reinterpret_cast<unsigned long long*>(t->out_d + t->k5_off), t->bpt};
+                reinterpret_cast<unsigned long long*>(t->out_d + t->k5_off), t->bpt, t->k4_stride};
     KVF_CUDA(cudaMemcpy(t->desc, &td, sizeof(td), cudaMemcpyHostToDevice));
     return KVF_OK;
 }
 
 // Queue one request on t's ring (records staged so far travel with it).  *seq_out = its number.
 int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand, uint32_t m,
-         const kvf_evict_request* q, uint64_t* seq_out) {
+         const kvf_evict_request* q, uint64_t* seq_out, uint32_t k4_buf = 0) {
     kvf_engine* e = t->e;
     DeciderState& d = e->dec;
     if (int rc = ensure_cap(t, t->n > kMaxNodesSingleCta ? large_capacity(t->n) : t->n)) return rc;
@@ -658,6 +757,7 @@ int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand,
     r.n = t->n;
     r.n_recs = static_cast<uint32_t>(t->staged.size());
     r.m = m;
+    r.k4_buf = k4_buf;
     r.tree = t->desc;
     r.recs = recs_dev;
     r.bslot = inl ? nullptr : reinterpret_cast<const uint32_t*>(pd + off);
@@ -698,6 +798,21 @@ int post(kvf_tree* t, uint32_t type, const uint32_t* bslot, const int64_t* cand,
     }
     e->stats.decisions++;
     *seq_out = seq;
+    return KVF_OK;
+}
+
+// The staged K4 on the ring by itself (a reader needs its result, or the next request cannot
+// carry it).
+int post_staged_k4(kvf_tree* t) {
+    if (!t->k4_staged) return KVF_OK;
+    t->k4_staged = false;
+    const uint32_t b = t->k4_staged_buf;
+    uint64_t seq = 0;
+    if (int rc = post(t, REQ_PRIO, t->k4_bslot.data(), t->k4_cand.data(), static_cast<uint32_t>(t->k4_bslot.size()),
+                      nullptr, &seq, b))
+        return rc;
+    t->k4_seq[b] = seq;
+    t->k4_n[b] = t->n;
     return KVF_OK;
 }
 
@@ -847,13 +962,15 @@ int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_
         if (boundary_slot[b] >= t->n) return set_error(KVF_E_UNKNOWN_BOUNDARY_NODE, "boundary slot out of range");
         t->keys.note_rank(cand_rank[b]);
     }
-    if (t->k4_seq) {  // the previous K4's changes would be lost: the host must read them first
-        return set_error(KVF_E_INVALID_ARG, "kvf_tree_rank_changes not called for the previous K4");
+    if (t->k4_count == 2) {  // both result buffers hold unread changes: the host reads the oldest first
+        return set_error(KVF_E_INVALID_ARG, "two K4 results unread: call kvf_tree_rank_changes first");
     }
-    uint64_t seq = 0;
-    if (int rc = post(t, REQ_PRIO, boundary_slot, cand_rank, m, nullptr, &seq)) return rc;
-    t->k4_seq = seq;
-    t->k4_n = t->n;
+    if (int rc = post_staged_k4(t)) return rc;  // the previous one, in order
+    t->k4_staged_buf = (t->k4_head + t->k4_count) % 2;
+    t->k4_bslot.assign(boundary_slot, boundary_slot + m);
+    t->k4_cand.assign(cand_rank, cand_rank + m);
+    t->k4_staged = true;
+    t->k4_count++;
     return KVF_OK;
 }
 
@@ -861,16 +978,23 @@ int kvf_tree_rank_changes(kvf_tree* t, uint32_t* slots, int64_t* ranks, uint32_t
     if (!t || !n_changed) return set_error(KVF_E_INVALID_ARG, "null argument");
     KVF_GUARD(t->e);
     *n_changed = 0;
-    if (!t->k4_seq) return KVF_OK;
+    if (!t->k4_count) return KVF_OK;
     const auto t0 = std::chrono::steady_clock::now();
-    if (int rc = wait_req(t->e, t->k4_seq)) return rc;
-    const uint64_t* hdr = reinterpret_cast<const uint64_t*>(t->out_h);
+    const uint32_t b = t->k4_head;
+    if (t->k4_staged && t->k4_staged_buf == b) {
+        if (int rc = post_staged_k4(t)) return rc;
+    }
+    if (int rc = wait_req(t->e, t->k4_seq[b])) return rc;
+    const char* o = t->out_h + b * t->k4_stride;
+    const uint64_t* hdr = reinterpret_cast<const uint64_t*>(o);
     const uint32_t cnt = static_cast<uint32_t>(hdr[0]);
     if (cnt > cap || (cnt && (!slots || !ranks))) return set_error(KVF_E_INVALID_ARG, "rank-change buffer too small");
-    std::memcpy(slots, t->out_h + kHeaderBytes, cnt * 4ull);
-    std::memcpy(ranks, t->out_h + kHeaderBytes + ((t->k4_n * 4ull + 15) & ~15ull), cnt * 8ull);
+    std::memcpy(slots, o + kHeaderBytes, cnt * 4ull);
+    std::memcpy(ranks, o + kHeaderBytes + ((t->k4_n[b] * 4ull + 15) & ~15ull), cnt * 8ull);
     *n_changed = cnt;
-    t->k4_seq = 0;
+    t->k4_seq[b] = 0;
+    t->k4_head = (b + 1) % 2;
+    t->k4_count--;
     t->e->stats.decision_call_us +=
         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
     return KVF_OK;
@@ -887,6 +1011,7 @@ int kvf_tree_victims(kvf_tree* t, const kvf_evict_request* req, uint32_t* out_sl
     uint32_t cnt = 0;
     if (t->n > kMaxNodesSingleCta) {  // device-wide path: records first, then the grid kernels
         uint64_t seq = 0;
+        if (int rc = post_staged_k4(t)) return rc;  // its ranks first (a one-shot launch)
         if (int rc = post(t, REQ_APPLY, nullptr, nullptr, 0, nullptr, &seq)) return rc;
         LargeArrays a{t->mir.parent, t->mir.status, t->mir.lock, t->mir.rank, t->mir.time,
                       t->mir.seq,    t->mir.id,     t->mir.tokens, t->mir.backed, t->n};
@@ -896,7 +1021,17 @@ int kvf_tree_victims(kvf_tree* t, const kvf_evict_request* req, uint32_t* out_sl
         *out_count = cnt;
     } else if (t->n > 1 && req->needed) {
         uint64_t seq = 0;
-        if (int rc = post(t, REQ_VICTIMS, nullptr, nullptr, 0, req, &seq)) return rc;
+        if (t->k4_staged) {  // the queued K4 and this K5 in one ring slot
+            t->k4_staged = false;
+            const uint32_t b = t->k4_staged_buf;
+            if (int rc = post(t, REQ_PRIO_VICTIMS, t->k4_bslot.data(), t->k4_cand.data(),
+                              static_cast<uint32_t>(t->k4_bslot.size()), req, &seq, b))
+                return rc;
+            t->k4_seq[b] = seq;
+            t->k4_n[b] = t->n;
+        } else if (int rc = post(t, REQ_VICTIMS, nullptr, nullptr, 0, req, &seq)) {
+            return rc;
+        }
         if (int rc = wait_req(e, seq)) return rc;
         const char* o = t->out_h + t->k5_off;
         const uint64_t* hdr = reinterpret_cast<const uint64_t*>(o);
@@ -923,6 +1058,9 @@ int kvf_decider_hold(kvf_engine* e, int32_t hold) {
     e->dec.hold = hold != 0;
     if (!hold) decider_quiesce(e);          // leave now (its queue is served first)
     else if (e->dec.running && !e->dec.disabled) decider_quiesce(e);  // relaunched without an idle limit
+    // a held decider starts now, ahead of the run's first request: launched later it would
+    // queue for an SM behind whatever bulk grid (a prompt's payload fill, a K1) is running
+    if (hold && !e->dec.disabled && !e->dec.running) return launch_resident(e, e->dec.posted + 1);
     return KVF_OK;
 }
 

@@ -31,12 +31,14 @@ for label, env in (("resident", "1"), ("oneshot", "0")):
     r = runs[-1]
     res[label] = {
         "decision_us_per_agent_step": round(statistics.median(x["decision_us_total"] / x["arrivals"] for x in runs), 2),
+        "decision_excl_issue_us_per_agent_step": round(statistics.median(
+            (x["decision_us_total"] - x["decision_issue_us"]) / x["arrivals"] for x in runs), 2),
         "arrival_us_median": round(statistics.median(x["us"] for x in rows), 2),
         "priorities_us_median": round(statistics.median(x["priorities_us"] for x in rows), 2),
         "schedule_us_median": round(statistics.median(x["schedule_us"] for x in rows), 2),
         "prefetch_us_median": round(statistics.median(x["prefetch_us"] for x in rows), 2),
         "arrivals": n,
-        "k4_calls": r["priority_calls"], "k4_us_total": round(r["priority_us"], 1), "k4_join_us": round(r["k4_join_us"], 1),
+        "k4_calls": r["priority_calls"], "k4_issued": r["priority_issued"], "k4_us_total": round(r["priority_us"], 1), "k4_join_us": round(r["k4_join_us"], 1),
         "k5_calls": r["evict_calls"], "k5_us_total": round(r["k5_us"], 1), "apply_us": round(r["apply_us"], 1),
         "k1_k2_issue_us": round(r["issue_us"], 1), "resident_served": r["resident_served"],
         "oneshot_served": r["oneshot_served"], "resident_launches": r["resident_launches"],

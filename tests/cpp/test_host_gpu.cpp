@@ -172,6 +172,72 @@ TEST("evict: leaves before parents, a freed parent follows in the same pass; loc
     }
 }
 
+TEST("queued K4: records shipped while it is pending keep its ranks; K5 behind it sees them; late join") {
+    // Two caches built the same way: A joins every K4 at once (the reference's synchronous
+    // set_agent_priorities), B leaves it queued while locks and an eviction's status changes
+    // ship records (KVF_REC_KEEP_RANK), then joins at the end.  Victims and dumps must agree.
+    std::mt19937_64 rng(7);
+    for (int trial = 0; trial < 40; ++trial) {
+        Rig ra, rb;
+        std::vector<TokenSeq> used;
+        const size_t nseq = 4 + rng() % 12;
+        for (size_t k = 0; k < nseq; ++k) {
+            TokenSeq s;
+            const size_t len = 2 + rng() % 6;
+            for (size_t t = 0; t < len; ++t) s.push_back(static_cast<TokenId>(1 + rng() % 4));
+            used.push_back(s);
+            ra.put(s, 1.0 + k);
+            rb.put(s, 1.0 + k);
+        }
+        std::vector<std::pair<AgentId, std::pair<TokenSeq, size_t>>> marks;
+        for (size_t a = 0, na = 1 + rng() % 5; a < na; ++a) {
+            const TokenSeq& s = used[rng() % used.size()];
+            marks.push_back({AgentId{0, "agent" + std::to_string(a)}, {s, 1 + rng() % s.size()}});
+        }
+        for (auto& m : marks) {
+            ra.cache.mark_fixed_boundary(m.first, m.second.first, m.second.second);
+            rb.cache.mark_fixed_boundary(m.first, m.second.first, m.second.second);
+        }
+        StepMap steps;
+        for (auto& m : marks)
+            if (rng() % 4) steps[m.first] = static_cast<StepValue>(rng() % 6);
+        ra.cache.set_agent_priorities(steps);
+        rb.cache.set_agent_priorities_async(steps);
+        CHECK(rb.cache.priorities_pending());
+        // lock one sequence's path in both (its nodes ship lock records while B's K4 is queued)
+        const TokenSeq& locked = used[rng() % used.size()];
+        MatchResult ma = ra.cache.peek_prefix(locked), mb = rb.cache.peek_prefix(locked);
+        REQUIRE(!ma.path.empty() && !mb.path.empty());
+        ra.cache.lock_root_path(ma.path.back());
+        rb.cache.lock_root_path(mb.path.back());
+        const TierMode mode = trial % 2 ? TierMode::Offload : TierMode::Discard;
+        const EvictRequest req{Bytes(1 + rng() % 12) * kBpt, EvictionPolicy::WorkflowAware, mode, {}};
+        EvictOutcome oa = ra.cache.evict(req, ra.tier, 50.0);
+        EvictOutcome ob = rb.cache.evict(req, rb.tier, 50.0);
+        CHECK(rb.cache.priorities_pending());  // K5 ran behind the queued K4 without a join
+        REQUIRE(oa.victims.size() == ob.victims.size());
+        for (size_t k = 0; k < oa.victims.size(); ++k) {
+            CHECK(oa.victims[k].node_id == ob.victims[k].node_id);
+            CHECK(oa.victims[k].immediate == ob.victims[k].immediate);
+        }
+        // a second eviction ships the first one's status records, still under the queued K4
+        EvictOutcome oa2 = ra.cache.evict(req, ra.tier, 51.0);
+        EvictOutcome ob2 = rb.cache.evict(req, rb.tier, 51.0);
+        REQUIRE(oa2.victims.size() == ob2.victims.size());
+        for (size_t k = 0; k < oa2.victims.size(); ++k) CHECK(oa2.victims[k].node_id == ob2.victims[k].node_id);
+        ra.cache.unlock_root_path(ma.path.back());
+        rb.cache.unlock_root_path(mb.path.back());
+        rb.cache.join_priorities();
+        CHECK(!rb.cache.priorities_pending());
+        CHECK(ra.cache.dump() == rb.cache.dump());
+        for (Rig* r : {&ra, &rb})  // fence the write-backs (K2) before the rigs go
+            while (!r->ev.empty()) {
+                Event done = r->ev.pop();
+                r->tier.complete(done.id, done.time);
+            }
+    }
+}
+
 TEST("offload eviction moves real bytes; a backed copy makes the next eviction instant") {
     Rig r;
     r.put({1, 11, 12}, 1.0);

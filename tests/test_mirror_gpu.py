@@ -344,3 +344,39 @@ def test_mirror_grows_past_its_capacity_with_a_k4_pending(eng):
         tree["depth"] = depth_from_parent(parent)
         wi, wa, wimm, wpend = eng.victims(tree, 400, True, True)
         assert slots.tolist() == wi.tolist() and acts.tolist() == wa.tolist() and (imm, pend) == (wimm, wpend)
+
+
+def test_two_queued_k4_results_read_in_order_across_a_mirror_move(eng):
+    """Two K4 requests queued back to back (the engine keeps two result buffers); a third is
+    refused until the oldest is read.  The results, read oldest first and applied in order,
+    give the second K4's ranks -- also when the mirror is reallocated while both are unread."""
+    from paper_2507_07400_b200.engine import Tree
+    rng = np.random.default_rng(11)
+    n = 3000
+    parent = np.zeros(n, dtype=np.int32)
+    parent[0] = -1
+    for i in range(1, n):
+        parent[i] = rng.integers(0, i)
+    suffix = 4611686018427387903
+    recs = [{"slot": i, "parent": int(parent[i]), "lock": 1 if i == 0 else 0, "status": 0, "backed": 0,
+             "rank": suffix, "time": float(i), "seq": i, "id": i, "tokens": 1} for i in range(n)]
+    for grow in (False, True):
+        with Tree(eng, 5) as t:
+            m = 600 if grow else n
+            t.update(recs[:m])
+            b1, b2 = [int(x) for x in rng.integers(1, m, size=5)], [int(x) for x in rng.integers(1, m, size=4)]
+            c1, c2 = [3, 1, 4, 1, 5], [2, 7, 1, 8]
+            t.priorities(b1, c1)
+            t.priorities(b2, c2)
+            with pytest.raises(Exception):
+                t.priorities(b1, c1)   # both result buffers unread
+            if grow:
+                t.update(recs[m:])     # the next request reallocates the mirror (1024 -> 3000+ slots)
+                t.victims(needed=1, workflow_aware=True, offload=False)
+            host = np.full(m, suffix, dtype=np.int64)
+            for _ in range(2):
+                for s, r in t.rank_changes().items():
+                    host[s] = r
+            assert t.rank_changes() == {}
+            want = eng.priority(parent[:m], b2, c2)
+            assert host[1:].tolist() == [int(x) for x in want[1:]]
