@@ -51,8 +51,10 @@ def build(e, lens, rng, piece=None):
     return seqs
 
 
-def step(e, seqs, q, out, group, layers, scale):
+def step(e, seqs, q, out, group, layers, scale, queued=False):
     seqs = e.attend_runs(seqs)
+    if queued:  # hold the compute stream while the calls are enqueued: each job = device time
+        e.compute_spin(3_000_000, 1)
     jobs = [e.attend(layer, group, q.data_ptr(), seqs, out.data_ptr(), scale) for layer in range(layers)]
     ms = e.span_ms(jobs[0], jobs[-1])
     per = [e.elapsed_ms(j) for j in jobs]
@@ -89,6 +91,9 @@ def run(name, kv_local, group, lens, piece=None, steps=5, layers=32):
         ms, per = step(e, seqs, q, out, group, layers, scale)
         spans.append(ms)
         pers += per
+    qpers = []
+    for _ in range(steps):
+        qpers += step(e, seqs, q, out, group, layers, scale, queued=True)[1]
     chained = [step_chained(e, seqs, q, out, group, layers, scale) for _ in range(steps + 2)][2:]
     bytes_layer = total * 2 * e.tpb
     # compaction comparator: K3 gathers every sequence (all layers) into staging, then attend
@@ -114,6 +119,9 @@ def run(name, kv_local, group, lens, piece=None, steps=5, layers=32):
             "step_ms": round(step_ms, 4), "layer_call_ms_median": round(layer_ms, 4),
             "achieved_GBps": round(gbs, 1), "step_GBps": round(bytes_layer * layers / (step_ms * 1e-3) / 1e9, 1),
             "hbm_peak_GBps": peak, "peak_source": src, "frac": round(gbs / peak, 4),
+            # the same single-layer calls enqueued behind earlier work (a decoder's steady state)
+            "queued_layer_call_us_median": round(float(np.median(qpers)) * 1e3, 2),
+            "queued_frac": round(bytes_layer / (float(np.median(qpers)) * 1e-3) / 1e9 / peak, 4),
             "chained_step_ms": round(min(chained), 4),
             "chained_layer_us": round(min(chained) / layers * 1e3, 2),
             "chained_GBps": round(bytes_layer * layers / (min(chained) * 1e-3) / 1e9, 1),
