@@ -288,6 +288,11 @@ int kvf_tree_set_hints(kvf_tree* t, uint32_t hints);
  * returns the slots whose rank it changed (at most the tree's slot count entries), relative
  * to the ranks the K4 before it left -- applying each result in order gives the latest ranks. */
 int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m);
+/* The same K4, staged instead of posted: it travels in the ring slot of the tree's next request
+ * -- with the next kvf_tree_victims in ONE slot (records, K4, K5: one poll, one serve) -- or
+ * alone when kvf_tree_rank_changes / another K4 needs it first.  For a caller that always
+ * decides next (RadixCache::evict after set_agent_priorities_async). */
+int kvf_tree_stage_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m);
 int kvf_tree_rank_changes(kvf_tree* t, uint32_t* slots, int64_t* ranks, uint32_t cap, uint32_t* n_changed);
 /* K5 over the mirror (evict's victim order and actions); victims as slots.  Synchronous. */
 int kvf_tree_victims(kvf_tree* t, const kvf_evict_request* req, uint32_t* out_slot, uint8_t* out_action,

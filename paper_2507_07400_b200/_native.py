@@ -134,6 +134,7 @@ _ENGINE_SIGS = {
     "kvf_tree_set_hints": (C.c_int, [C.c_void_p, C.c_uint32]),
     "kvf_tree_update": (C.c_int, [C.c_void_p, C.POINTER(NodeRec), C.c_uint32]),
     "kvf_tree_priorities": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.c_uint32]),
+    "kvf_tree_stage_priorities": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.c_uint32]),
     "kvf_tree_rank_changes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int64), C.c_uint32,
                                         C.POINTER(C.c_uint32)]),
     "kvf_tree_victims": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint8), C.c_uint32,

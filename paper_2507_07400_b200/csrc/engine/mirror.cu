@@ -955,7 +955,7 @@ int kvf_tree_update(kvf_tree* t, const kvf_node_rec* recs, uint32_t n) {
     return KVF_OK;
 }
 
-int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m) {
+int kvf_tree_stage_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m) {
     if (!t || (m && (!boundary_slot || !cand_rank))) return set_error(KVF_E_INVALID_ARG, "null argument");
     KVF_GUARD(t->e);
     for (uint32_t b = 0; b < m; ++b) {
@@ -972,6 +972,12 @@ int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_
     t->k4_staged = true;
     t->k4_count++;
     return KVF_OK;
+}
+
+int kvf_tree_priorities(kvf_tree* t, const uint32_t* boundary_slot, const int64_t* cand_rank, uint32_t m) {
+    if (int rc = kvf_tree_stage_priorities(t, boundary_slot, cand_rank, m)) return rc;
+    KVF_GUARD(t->e);
+    return post_staged_k4(t);  // on the ring now: it runs while the caller goes on
 }
 
 int kvf_tree_rank_changes(kvf_tree* t, uint32_t* slots, int64_t* ranks, uint32_t cap, uint32_t* n_changed) {
