@@ -230,11 +230,12 @@ int kvfh_sim_run(kvfh_sim* s) {
                           "{\"t\":\"req\",\"id\":%" PRIu64 ",\"client\":%u,\"agent\":%s,\"seq\":%" PRIu64 ",\"iter\":%u,"
                           "\"measured\":%d,\"arrival\":%s,\"prefill_start\":%s,\"first_token\":%s,\"done\":%s,"
                           "\"prompt\":%" PRIu64 ",\"matched\":%" PRIu64 ",\"loaded\":%" PRIu64 ",\"recomputed\":%" PRIu64
-                          ",\"fixed\":%" PRIu64 ",\"output\":%" PRIu64 ",\"loaded_bytes\":%" PRIu64 ",\"stall\":%s}\n",
+                          ",\"fixed\":%" PRIu64 ",\"output\":%" PRIu64 ",\"loaded_bytes\":%" PRIu64 ",\"stall\":%s%s}\n",
                           t.request_id, t.client, js(t.agent).c_str(), t.arrival_seq, t.iteration, t.measured ? 1 : 0,
                           jd(t.arrival).c_str(), jd(t.prefill_start).c_str(), jd(t.first_token).c_str(),
                           jd(t.done).c_str(), t.prompt_tokens, t.matched_tokens, t.loaded_tokens, t.recomputed_tokens,
-                          t.fixed_tokens, t.output_tokens, t.loaded_bytes, jd(t.stall_seconds).c_str());
+                          t.fixed_tokens, t.output_tokens, t.loaded_bytes, jd(t.stall_seconds).c_str(),
+                          t.load_wait_seconds < 0 ? "" : (",\"load_wait\":" + jd(t.load_wait_seconds)).c_str());
             o += b;
         }
         std::snprintf(b, sizeof b,

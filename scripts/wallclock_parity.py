@@ -88,6 +88,7 @@ def run_one(name, reps=1):
         # steps the reference served by prefetch: measured, nothing loaded reactively by the step itself
         served = [r for r in trace if r["t"] == "req" and r["measured"] and ref_reqs.get(r["id"], {}).get("loaded_bytes", 1) == 0]
         stalls_us = sorted(1e6 * r["stall"] for r in served)
+        waits_us = sorted(1e6 * r["load_wait"] for r in served)
         reactive = [r for r in trace if r["t"] == "req" and r["measured"] and r["loaded_bytes"] > 0]
         runs.append({
             "issue_order_equal": jobs == ref_jobs,
@@ -103,6 +104,11 @@ def run_one(name, reps=1):
                                          "p90": round(stalls_us[int(0.9 * (len(stalls_us) - 1))], 2) if stalls_us else None,
                                          "zero": sum(1 for s in stalls_us if s == 0.0),
                                          "under_100us": sum(1 for s in stalls_us if s < 100.0)},
+            # the prefix-miss stall proper: GPU-timed waits of the step's prefill on KV loads
+            "prefetch_served_load_wait_us": {"max": round(max(waits_us), 2) if waits_us else None,
+                                             "zero": sum(1 for s in waits_us if s == 0.0),
+                                             "nonzero": [round(s, 2) for s in waits_us if s != 0.0][:10]},
+            "reactive_load_wait_ms": [round(1e3 * r["load_wait"], 3) for r in reactive],
             "reactive_steps": len(reactive),
             "reactive_stall_ms": [round(1e3 * r["stall"], 3) for r in reactive],
             "prefetch_jobs": res["prefetch_jobs"], "reactive_jobs": res["reactive_jobs"],

@@ -32,3 +32,9 @@ def test_wall_clock_decisions_equal_reference(cfg):
     st = run["prefetch_served_stall_us"]
     assert run["prefetch_served_steps"] == 37
     assert st["median"] < 250 and st["max"] < 2000, st
+    # north_star: zero prefix-miss stalls on the prefetch-served steps -- none of them was held
+    # for KV on the wire or on the host, and no prefill's compute stream waited on a load
+    # (GPU-timed); the rest of `stall` is dispatch latency.  The reactive steps do wait.
+    lw = run["prefetch_served_load_wait_us"]
+    assert lw["zero"] == 37 and lw["max"] == 0.0, lw
+    assert all(w > 0 for w in run["reactive_load_wait_ms"])
